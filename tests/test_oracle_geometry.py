@@ -1,0 +1,282 @@
+"""Pins for oracle O1-O5 (geometry, marginal projection, AABB, lists).
+
+Each test checks the oracle against something other than itself: SPEC worked
+examples (tests/golden/spec_examples.json), scipy quadrature / rotation
+routines, closed forms (Gaussian mass), invariants and brute force.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import integrate
+from scipy.spatial.transform import Rotation
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def sigma_ref(q, s):
+    """Independent covariance: scipy rotation (scalar-last quaternion) and numpy products."""
+    R = Rotation.from_quat([q[1], q[2], q[3], q[0]]).as_matrix()
+    return R @ np.diag(np.exp(2 * np.asarray(s))) @ R.T
+
+
+def one_gauss(mu, s, q, rho):
+    return (np.array([[*mu, rho]], float), np.array([[*s, 0.0]], float), np.array([q], float))
+
+
+# ---------------------------------------------------------------- O1
+@pytest.mark.parametrize("ex", GOLD["quat_to_rotation"], ids=lambda e: e["cite"])
+def test_quat_rotation_spec_examples(orc, ex):
+    ok, R, _, _, _, _ = orc.gauss(ex["quat"], [0, 0, 0])
+    assert ok
+    if "R" in ex:
+        assert np.abs(R - np.array(ex["R"])).max() <= ex["tol"]
+    else:
+        assert np.abs(R @ np.array(ex["apply"]) - np.array(ex["expect"])).max() <= ex["tol"]
+
+
+def test_quat_rotation_matches_scipy_and_is_proper(orc):
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        q = rng.standard_normal(4) * rng.uniform(0.2, 3.0)
+        ok, R, _, _, qn, qh = orc.gauss(q, [0, 0, 0])
+        assert ok and abs(qn - np.linalg.norm(q)) < 1e-14 * qn
+        Rs = Rotation.from_quat([q[1], q[2], q[3], q[0]]).as_matrix()
+        assert np.abs(R - Rs).max() < 1e-14
+        assert np.abs(R.T @ R - np.eye(3)).max() < 1e-14
+        assert abs(np.linalg.det(R) - 1.0) < 1e-14
+
+
+@pytest.mark.parametrize("ex", GOLD["assemble_covariance"], ids=lambda e: e["cite"])
+def test_covariance_spec_examples(orc, ex):
+    ok, _, S, det, _, _ = orc.gauss(ex["quat"], ex["log_scales"])
+    assert ok and np.abs(S - np.array(ex["Sigma"])).max() <= ex["tol"]
+    assert abs(det - np.linalg.det(np.array(ex["Sigma"]))) < 1e-9
+
+
+def test_covariance_eigen_and_det(orc):
+    rng = np.random.default_rng(2)
+    for _ in range(50):
+        q, s = rng.standard_normal(4), rng.uniform(-1, 1, 3)
+        ok, _, S, det, _, _ = orc.gauss(q, s)
+        assert ok
+        assert np.abs(S - sigma_ref(q, s)).max() < 1e-13 * np.abs(S).max()
+        ev = np.sort(np.linalg.eigvalsh(S))
+        assert np.allclose(ev, np.sort(np.exp(2 * s)), rtol=1e-12)
+        assert abs(det - np.linalg.det(S)) < 1e-12 * det
+        np.linalg.cholesky(S)
+
+
+def test_degenerate_quaternion(orc):
+    assert not orc.gauss([0, 0, 0, 0], [0, 0, 0])[0]
+    assert not orc.gauss([np.nan, 0, 0, 1], [0, 0, 0])[0]
+
+
+# ---------------------------------------------------------------- O2 amp
+@pytest.mark.parametrize("ex", GOLD["marginal_amplitude"], ids=lambda e: e["cite"])
+def test_marginal_amplitude_spec(orc, ex):
+    if "sigmas" in ex:
+        sig, rho = np.array(ex["sigmas"]), ex["rho"]
+        expect = rho * sig[2] * math.sqrt(2 * math.pi)
+    else:
+        sig, rho, expect = np.ones(3), 1.0, ex["amp"]
+    params = one_gauss([0, 0, 0], np.log(sig), [1, 0, 0, 0], rho)
+    _, _, sp = orc.splats(params, np.eye(3).reshape(1, 9), np.zeros((1, 2)), 16, 1.0)
+    assert abs(sp[0, 0, 6] - expect) <= ex["tol"] * expect
+
+
+def test_amplitude_is_line_integral(orc):
+    """O2 closed form vs 1D adaptive quadrature of G along the camera z axis,
+    for random anisotropic Gaussians, poses and pixels (App. A.2)."""
+    rng = np.random.default_rng(3)
+    D, px = 16, 1.5
+    for trial in range(12):
+        mu = rng.uniform(-3, 3, 3)
+        s = rng.uniform(-0.2, 0.8, 3)
+        q = rng.standard_normal(4)
+        rho = rng.uniform(0.5, 2)
+        P = Rotation.random(random_state=trial).as_matrix()
+        t = rng.uniform(-2, 2, 2)
+        params = one_gauss(mu, s, q, rho)
+        img = orc.project(params, P.reshape(1, 9), t.reshape(1, 2), D, px, masked=False)[0]
+        Sinv = np.linalg.inv(sigma_ref(q, s))
+        for (u, v) in [(8, 8), (6, 9), (int(rng.integers(0, D)), int(rng.integers(0, D)))]:
+            x, y = (u - D / 2) * px, (v - D / 2) * px
+
+            def G(z):
+                xw = P @ (np.array([x, y, z]) - np.array([t[0], t[1], 0.0]))  # world = W^T (cam - t)
+                d = xw - mu
+                return rho * math.exp(-0.5 * d @ Sinv @ d)
+
+            val, err = integrate.quad(G, -60, 60, epsabs=1e-14, epsrel=1e-13, limit=400)
+            assert abs(img[v, u] - val) <= 1e-11 * max(1.0, abs(val)), (trial, u, v, img[v, u], val)
+
+
+def test_spec_centre_pixel_and_fourfold_symmetry(orc):
+    ex = GOLD["project"][0]
+    D, px = ex["D"], ex["px"]
+    params = one_gauss([0, 0, 0], [0, 0, 0], [1, 0, 0, 0], 1.0)
+    img = orc.project(params, np.eye(3).reshape(1, 9), np.zeros((1, 2)), D, px, masked=False)[0]
+    assert abs(img[D // 2, D // 2] - ex["value"]) < ex["tol"]
+    c = img[1:, 1:]  # centre at index D/2 -> symmetric on [1, D-1]
+    assert np.abs(c - c[::-1, :]).max() < 1e-15 and np.abs(c - c.T).max() < 1e-15
+
+
+def test_mass_conservation_poisson(orc):
+    """sum_pixels I_inf px^2 = rho (2 pi)^{3/2} |Sigma|^{1/2} (north star; Poisson
+    summation error <= 2 exp(-2 pi^2 sigma^2/px^2) per axis, sigma >= 1.5 px)."""
+    rng = np.random.default_rng(4)
+    D, px = 48, 1.0
+    for trial in range(6):
+        s = np.log(rng.uniform(1.5, 2.5, 3))
+        q, rho = rng.standard_normal(4), rng.uniform(0.5, 2)
+        mu = rng.uniform(-2, 2, 3)
+        P = Rotation.random(random_state=10 + trial).as_matrix()
+        params = one_gauss(mu, s, q, rho)
+        img = orc.project(params, P.reshape(1, 9), np.zeros((1, 2)), D, px, masked=False)[0]
+        mass = img.sum() * px * px
+        expect = rho * (2 * math.pi) ** 1.5 * math.exp(s.sum())
+        assert abs(mass - expect) < 2e-8 * expect
+
+
+def test_rotation_invariance_isotropic(orc):
+    D, px = 24, 1.3
+    params = one_gauss([0, 0, 0], np.log([1.4] * 3), [0.3, 0.1, -0.5, 0.2], 1.1)
+    ref = orc.project(params, np.eye(3).reshape(1, 9), np.zeros((1, 2)), D, px, masked=False)[0]
+    for seed in range(5):
+        P = Rotation.random(random_state=seed).as_matrix()
+        img = orc.project(params, P.reshape(1, 9), np.zeros((1, 2)), D, px, masked=False)[0]
+        assert np.abs(img - ref).max() < 1e-14 * np.abs(ref).max()
+
+
+def test_inplane_180_symmetry(orc):
+    """Pose rotated 180 deg about the beam axis -> image rotated 180 deg."""
+    rng = np.random.default_rng(5)
+    D, px, N = 20, 1.0, 7
+    params = (np.c_[rng.uniform(-4, 4, (N, 3)), rng.uniform(0.5, 1.5, N)],
+              np.c_[np.log(rng.uniform(0.8, 1.6, (N, 3))), np.zeros(N)], rng.standard_normal((N, 4)))
+    P = Rotation.random(random_state=7).as_matrix()
+    Rz = np.diag([-1.0, -1.0, 1.0])
+    for masked in (False, True):
+        a = orc.project(params, P.reshape(1, 9), np.zeros((1, 2)), D, px, masked=masked)[0]
+        b = orc.project(params, (P @ Rz).reshape(1, 9), np.zeros((1, 2)), D, px, masked=masked)[0]
+        assert np.abs(a[1:, 1:] - b[1:, 1:][::-1, ::-1]).max() < 1e-13 * np.abs(a).max()
+
+
+def test_projection_equals_volume_z_sum(orc):
+    """Dense z-quadrature: sum_z V_inf(x,y,z) vs = I_inf under the
+    identity pose (Poisson summation along z; sigma >= 1.5 voxel)."""
+    rng = np.random.default_rng(6)
+    Dv, vs, N = 40, 1.0, 4
+    params = (np.c_[rng.uniform(-2, 2, (N, 3)), rng.uniform(0.5, 1.5, N)],
+              np.c_[np.log(rng.uniform(1.5, 2.2, (N, 3))), np.zeros(N)], rng.standard_normal((N, 4)))
+    vol = orc.volume(params, Dv, vs, masked=False)          # [z][y][x]
+    img = orc.project(params, np.eye(3).reshape(1, 9), np.zeros((1, 2)), Dv, vs, masked=False)[0]
+    zsum = vol.sum(0) * vs
+    # the z extent [-20, 19] vs covers > 8 sigma of every kernel
+    assert np.abs(zsum - img).max() < 1e-8 * np.abs(img).max()
+
+
+def _random_case(rng, N, D, px, sig_px=(0.6, 1.4), spread=0.45):
+    mu = rng.uniform(-spread * D * px, spread * D * px, (N, 3))
+    s = np.log(rng.uniform(*sig_px, (N, 3)) * px)
+    q = rng.standard_normal((N, 4))
+    rho = rng.uniform(0.5, 1.5, N)
+    return (np.c_[mu, rho], np.c_[s, np.zeros(N)], q)
+
+
+def test_masked_vs_unmasked_tail_bound(orc):
+    """|I_inf - I| <= exp(-k^2/2) sum_{j: pixel outside AABB_j} |amp_j| (rigorous: Q >= k^2 outside)."""
+    rng = np.random.default_rng(7)
+    D, px, N, B = 24, 1.2, 30, 2
+    params = _random_case(rng, N, D, px)
+    rot = np.stack([Rotation.random(random_state=s).as_matrix().reshape(9) for s in range(B)])
+    shift = rng.uniform(-2, 2, (B, 2))
+    full = orc.project(params, rot, shift, D, px, masked=False)
+    msk = orc.project(params, rot, shift, D, px, masked=True)
+    aabb, vis, sp = orc.splats(params, rot, shift, D, px)
+    for i in range(B):
+        for v in range(D):
+            for u in range(D):
+                inside = vis[i].astype(bool) & (aabb[i, :, 0] <= u) & (u <= aabb[i, :, 1]) & \
+                    (aabb[i, :, 2] <= v) & (v <= aabb[i, :, 3])
+                bound = math.exp(-4.5) * np.abs(sp[i, ~inside, 6]).sum()
+                assert abs(full[i, v, u] - msk[i, v, u]) <= bound * (1 + 1e-12) + 1e-15
+
+
+def test_linearity_additivity_permutation(orc):
+    rng = np.random.default_rng(8)
+    D, px, N = 20, 1.0, 12
+    mr, ls, q = _random_case(rng, N, D, px)
+    rot = Rotation.random(random_state=3).as_matrix().reshape(1, 9)
+    sh = np.array([[0.3, -0.7]])
+    base = orc.project((mr, ls, q), rot, sh, D, px)
+    mr2 = mr.copy(); mr2[:, 3] *= 2.0
+    assert np.array_equal(orc.project((mr2, ls, q), rot, sh, D, px), 2.0 * base)   # exact in fp64
+    a = orc.project((mr[:5], ls[:5], q[:5]), rot, sh, D, px)
+    b = orc.project((mr[5:], ls[5:], q[5:]), rot, sh, D, px)
+    assert np.abs(a + b - base).max() < 1e-13 * np.abs(base).max()
+    perm = rng.permutation(N)
+    c = orc.project((mr[perm], ls[perm], q[perm]), rot, sh, D, px)
+    assert np.abs(c - base).max() < 1e-13 * np.abs(base).max()
+
+
+def test_aabb_matches_parametric_ellipse(orc):
+    """O3 pin: the integer box is the tightest box holding the k=3 ellipse.
+    Ellipse sampled parametrically from an independent Cholesky factor of the
+    posed covariance (scipy rotation, numpy products)."""
+    rng = np.random.default_rng(9)
+    D, px, N, B, k = 32, 1.31, 40, 3, 3.0
+    mr, ls, q = _random_case(rng, N, D, px, spread=0.5)
+    rot = np.stack([Rotation.random(random_state=20 + s).as_matrix() for s in range(B)])
+    sh = rng.uniform(-3, 3, (B, 2))
+    aabb, vis, sp = orc.splats((mr, ls, q), rot.reshape(B, 9), sh, D, px, k=k)
+    th = np.linspace(0, 2 * np.pi, 20001)
+    checked = 0
+    for i in range(B):
+        W = rot[i].T
+        for j in range(N):
+            S = W @ sigma_ref(q[j], ls[j, :3]) @ W.T
+            L = np.linalg.cholesky(S[:2, :2])
+            m = (W @ mr[j, :3])[:2] + sh[i]
+            pts = m[:, None] + k * L @ np.stack([np.cos(th), np.sin(th)])
+            lo = pts.min(1) / px + D / 2
+            hi = pts.max(1) / px + D / 2
+            exp_lo = np.ceil(lo - 1e-9)  # sampled extreme is inside by <= 1e-8 px
+            exp_hi = np.floor(hi + 1e-9)
+            if np.any(np.abs(lo - np.round(lo)) < 1e-6) or np.any(np.abs(hi - np.round(hi)) < 1e-6):
+                continue  # near-integer bound: sampling cannot decide
+            elo = np.clip(exp_lo, 0, D).astype(int)
+            ehi = np.clip(exp_hi, -1, D - 1).astype(int)
+            visible = elo[0] <= ehi[0] and elo[1] <= ehi[1]
+            assert bool(vis[i, j]) == visible
+            if visible:
+                assert list(aabb[i, j]) == [elo[0], ehi[0], elo[1], ehi[1]], (i, j)
+                checked += 1
+    assert checked > 20
+
+
+@pytest.mark.parametrize("D,T", [(32, 16), (40, 16), (24, 8)])
+def test_lists_brute_force(orc, D, T):
+    """O4 lists equal a pure-Python scan of tile/box intersections, ascending j."""
+    rng = np.random.default_rng(D + T)
+    N, B, px = 60, 2, 1.0
+    params = _random_case(rng, N, D, px, sig_px=(0.6, 3.0), spread=0.6)
+    rot = np.stack([Rotation.random(random_state=40 + s).as_matrix().reshape(9) for s in range(B)])
+    sh = rng.uniform(-3, 3, (B, 2))
+    aabb, vis, _ = orc.splats(params, rot, sh, D, px)
+    tile_off, base, ids = orc.lists(aabb, vis, D, T)
+    nt = -(-D // T)
+    for i in range(B):
+        for t in range(nt * nt):
+            tu, tv = t % nt, t // nt
+            exp = [j for j in range(N) if vis[i, j] and aabb[i, j, 0] // T <= tu <= aabb[i, j, 1] // T
+                   and aabb[i, j, 2] // T <= tv <= aabb[i, j, 3] // T]
+            got = ids[base[i] + tile_off[i, t]: base[i] + tile_off[i, t + 1]]
+            assert list(got) == exp
+    # off-frame Gaussian appears in no tile
+    far = (np.array([[1e4, 0, 0, 1.0]]), np.zeros((1, 4)), np.array([[1.0, 0, 0, 0]]))
+    a2, v2, _ = orc.splats(far, rot[:1], sh[:1], D, px)
+    assert v2.sum() == 0
