@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""bench.py — throughput of one GEM training step on B200 (particle images/s).
+
+A "step" is one pass of the whole hot path over one
+batch of B particles per GPU: Gaussian prep, splat + cull/bin, per-tile lists,
+projection, cuFFT + fused CTF/loss, backward scatter, finalize, NCCL all-reduce
+of the N x 12 gradient (N>1) and the fused Adam update.  Workload: config R of
+BASELINE.json (EMPIAR-10028-shaped: N = 50,000 Gaussians, D = 256, px 1.31 A),
+synthetic seeded inputs, weak scaling (B per GPU fixed).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints ONE JSON line on rank 0.  Multi-GPU: launched by torch.distributed.run,
+one rank per GPU, NCCL; the timed region is bracketed by barrier + sync and the
+elapsed time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2509_25075_b200 import synth  # noqa: E402
+
+METRIC = "particle images/sec per train step (fwd+bwd) at D=256"
+SNR = 0.1
+# algorithmic FP32 FLOPs per useful (Gaussian, pixel) pair (FMA = 2 FLOPs)
+FLOP_FWD_PAIR = 12
+FLOP_BWD_PAIR = 25
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["gem", "reference"], default="gem")
+    ap.add_argument("--config", default="R", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--batch", type=int, default=128, help="particles per GPU per step")
+    ap.add_argument("--tile", type=int, default=16)
+    ap.add_argument("--state", default="steady", choices=["steady", "init"])
+    ap.add_argument("--ring", type=int, default=1024, help="distinct device-resident particles per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)), "measured"
+        except Exception:
+            pass
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def fp32_peak_tflops(sm_mhz):
+    """148 SMs x 128 FP32 lanes x 2 FLOP/FMA x clock (B200_PROFILING.md unit counts)."""
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu_id), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0])); mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU oracle
+def oracle_step_sample(w, n_particles, seed=7):
+    """One oracle training step (forward, backward, Adam) on n particles of workload w.
+    Returns seconds.  TEST/BASELINE infrastructure: the oracle as it stands."""
+    import oracle
+    mr, ls, q = synth.steady_model(w, 0)
+    rot, shift, ctf = synth.particles(w, n_particles, seed)
+    obs = synth.noise_images(w, n_particles, seed)
+    mr, ls, q, rot, shift, ctf, obs = synth.f32(mr, ls, q, rot, shift, ctf, obs)
+    px = float(np.float32(w.px))
+    t0 = time.perf_counter()
+    out = oracle.loss_grad((mr, ls, q), rot, shift, ctf, obs, w.D, px)
+    p = np.stack([mr, ls, q]).astype(np.float64)
+    z = np.zeros_like(p)
+    oracle.adam(p, oracle.grad_to_soa(out["grad"]), z, z, 1, [1e-3, 5e-3, 1e-3, 5e-2])
+    return time.perf_counter() - t0
+
+
+def cpu_cores():
+    env = os.environ.get("OMP_NUM_THREADS")
+    return int(env) if env else (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+
+
+def cpu_baseline(w, budget_s=15.0):
+    import oracle
+    oracle.lib()
+    t1 = oracle_step_sample(w, 1)
+    n = int(max(1, min(16, budget_s // max(t1, 1e-3))))
+    t = oracle_step_sample(w, n) if n > 1 else t1
+    return {"value": n / t, "unit": "particles/s", "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"{n} particle(s) of workload {w.name} (N={w.N}, D={w.D}): full fp64 forward "
+                      f"(masked sum over every Gaussian x pixel), DFT CTF/loss, backward, Adam; {t:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the fp64 oracle as it stands on the host cores, timed on a
+    bounded sample per step (rank 0 only)."""
+    if rank != 0:
+        return 0
+    w = synth.CONFIGS[args.config]
+    t1 = oracle_step_sample(w, 1)
+    budget = 150.0
+    steps = args.steps
+    warm = min(args.warmup, 1)
+    per_step = 1
+    if (steps + warm) * t1 > budget:
+        steps = max(1, int(budget // t1) - warm)
+    for _ in range(warm):
+        oracle_step_sample(w, per_step, seed=11)
+    tt = 0.0
+    for k in range(steps):
+        tt += oracle_step_sample(w, per_step, seed=100 + k)
+    value = steps * per_step / tt
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world,
+            "steps": steps, "warmup": warm, "ms_per_step": 1e3 * tt / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{w.name}: N={w.N} Gaussians, D={w.D}, px={w.px} A", "batch_per_step": per_step,
+                       "requested_steps": args.steps},
+            "cpu_baseline": {"value": value, "unit": "particles/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": f"{per_step} particle per step x {steps} steps"},
+            "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2509_25075_b200 import gem
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    w = synth.CONFIGS[args.config]
+    B = args.batch
+    ring = max(args.ring // B, 1) * B
+    px = float(np.float32(w.px))
+    model = synth.steady_model if args.state == "steady" else synth.init_model
+    mr, ls, q = synth.f32(*model(w, 0))
+    params = gem.SoA.from_arrays(mr, ls, q, dev)
+    phantom = gem.SoA.from_arrays(*synth.f32(*synth.phantom(w, synth.seed_for(w.name, "phantom", 0))), dev)
+    cfg = gem.GemConfig(D=w.D, pixel_size=px, n_gauss=w.N, max_batch=B, tile=args.tile,
+                        lr_mean=1e-3 * w.ball_radius)
+
+    # device-resident ring of distinct synthetic particles (per-rank seeds)
+    rot_np, sh_np, ctf_np = synth.f32(*synth.particles(w, ring, 1000 + rank))
+    rot, shift, ctf = (torch.from_numpy(a).to(dev) for a in (rot_np, sh_np, ctf_np))
+    obs = torch.empty(ring, w.D, w.D, device=dev)
+    gen = gem.GemStep(gem.GemConfig(D=w.D, pixel_size=px, n_gauss=w.N, max_batch=B, tile=args.tile, cull_k=5.0), dev)
+    zeros = torch.zeros(B, w.D, w.D, device=dev)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    for s0 in range(0, ring, B):
+        sl = slice(s0, s0 + B)
+        gen.forward(phantom, rot[sl], shift[sl], ctf[sl], zeros, pred=obs[sl])
+        clean = obs[sl]
+        sd = clean.std(dim=(1, 2), keepdim=True) / SNR ** 0.5
+        obs[sl] = clean + sd * torch.randn(clean.shape, device=dev, generator=g)
+    del gen
+    torch.cuda.synchronize()
+
+    tr = gem.Trainer(cfg, params, dev)
+    sc = tr.step_ctx
+
+    def step(k, host=False, src=None):
+        s0 = (k * B) % ring
+        sl = slice(s0, s0 + B)
+        if host:
+            return tr.train_step(src[0][sl], src[1][sl], src[2][sl], src[3][sl], host=True, loss=src[4])
+        return tr.train_step(rot[sl], shift[sl], ctf[sl], obs[sl])
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    props = torch.cuda.get_device_properties(dev)
+    gpu_id = f"GPU-{props.uuid}" if getattr(props, "uuid", None) else local
+    stream = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = sc.launches
+    with ClockSampler(gpu_id) as clk:
+        sc.profile(True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record(stream)
+        for k in range(args.steps):
+            step(args.warmup + k)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        sc.profile(False)
+    launches = sc.launches - launches0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    kern = sc.profile_read()
+    st = sc.stats(check=False)
+    value = world * B * args.steps / (ms / 1e3)
+
+    # ---- e2e: same step through the C ABI with pinned HOST inputs (H2D inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hsrc = [a.cpu().pin_memory() for a in (rot, shift, ctf, obs)]
+        hsrc.append(torch.empty(B + 1, dtype=torch.float64).pin_memory())
+        step(0, host=True, src=hsrc)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.steps):
+            step(args.warmup + k, host=True, src=hsrc)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        _ = float(hsrc[4][-1])  # the step's loss, read on the host
+        e2e = {"value": world * B * args.steps / (ems / 1e3), "unit": "particles/s",
+               "h2d_bytes_per_step": B * (9 + 2 + 8 + w.D * w.D) * 4, "d2h_bytes_per_step": (B + 1) * 8}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peaks, peak_src = measured_peaks()
+    clocks = clk.summary()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    total_kernel_ms = sum(v[1] for v in kern.values())
+    kernels = {k: {"ms_per_step": v[1] / max(args.steps, 1), "launch_groups": v[0],
+                   "share": v[1] / total_kernel_ms if total_kernel_ms else None} for k, v in kern.items()}
+    pairs = int(st["pairs"])
+    dominant = max(kern, key=lambda k: kern[k][1]) if kern else None
+    roof = None
+    if dominant in ("render_fwd", "render_bwd"):
+        per_pair = FLOP_FWD_PAIR if dominant == "render_fwd" else FLOP_BWD_PAIR
+        avg_s = kern[dominant][1] / kern[dominant][0] / 1e3
+        achieved = per_pair * pairs / avg_s / 1e12
+        peak = fp32_peak_tflops(sm_max)
+        roof = {"bound": "alu", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "work_per_launch": f"{per_pair} FP32 FLOP x {pairs} useful (Gaussian, pixel) pairs",
+                "avg_launch_ms": avg_s * 1e3,
+                "peak_source": f"148 SMs x 128 FP32 lanes x 2 FLOP/FMA x {sm_max:.0f} MHz ({peak_src} sm_max_mhz)"}
+    elif dominant is not None:
+        roof = {"bound": "hbm", "kernel": dominant, "achieved": None, "peak": float(peaks.get("hbm_gbs", 6650.0)),
+                "unit": "GB/s", "frac": None, "traffic": None}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_baseline(w)
+        except Exception as e:  # oracle build failure must not kill the bench line
+            cpu = {"value": None, "unit": "particles/s", "cores": cpu_cores(), "kind": "oracle", "sample": f"failed: {e}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{w.name}: EMPIAR-10028-shaped, N={w.N} Gaussians, D={w.D}, px={w.px} A",
+                   "model_state": args.state, "batch_per_gpu": B, "global_batch": B * world, "tile": args.tile,
+                   "ring_particles_per_gpu": ring, "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2: per-step working set (splat records "
+                         f"{B * w.N * 32 / 1e6:.0f} MB + images) and a {ring}-particle ring "
+                         f"({ring * w.D * w.D * 4 / 1e6:.0f} MB) exceed the 126 MB L2",
+                   "useful_pairs_per_step": pairs, "list_entries_per_step": int(st["entries"])},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        "kernels": kernels,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,508 @@
+// gem_api.cu — the C ABI declared in include/gem.h: validation, workspace
+// carving, cuFFT plan management and the launch sequence of one step.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "gem_internal.cuh"
+
+namespace gem {
+void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, float2 *spec_hat, const float2 *spec_obs,
+                     float2 *spec_pred, double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
+                     int &launches);
+int ctf_loss_blocks(int D);
+}  // namespace gem
+
+using namespace gem;
+
+namespace {
+
+bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
+  if (!in) return false;
+  c = *in;
+  if (c.D < 2 || (c.D & 1) || c.D > 8192) return false;
+  if (!(c.pixel_size > 0.f) || !std::isfinite(c.pixel_size)) return false;
+  if (c.n_gauss < 1 || c.n_gauss > (1ll << 30)) return false;
+  if (c.max_batch < 1 || c.max_batch > 65535) return false;
+  if (c.cull_k == 0.f) c.cull_k = 3.f;
+  if (!(c.cull_k > 0.f) || !(c.tau >= 0.f)) return false;
+  if (c.tile == 0) c.tile = 16;
+  if (c.tile != 8 && c.tile != 16) return false;
+  if (c.beta1 == 0.f) c.beta1 = 0.9f;
+  if (c.beta2 == 0.f) c.beta2 = 0.999f;
+  if (c.eps == 0.f) c.eps = 1e-8f;
+  d.D = c.D;
+  d.T = c.tile;
+  d.nt = (c.D + c.tile - 1) / c.tile;
+  d.NT = d.nt * d.nt;
+  d.N = (int)c.n_gauss;
+  d.C = (d.N + kChunk - 1) / kChunk;
+  d.px = c.pixel_size;
+  d.k = c.cull_k;
+  d.tau = c.tau;
+  if (c.list_capacity <= 0)
+    c.list_capacity = (int64_t)c.max_batch * ((c.tile == 16 ? 6 : 12) * (int64_t)d.N + d.NT);
+  if (c.list_capacity > 0x7fffffffll) c.list_capacity = 0x7fffffffll;
+  d.cap = c.list_capacity;
+  return true;
+}
+
+bool make_plan(int D, int B, cufftType type, cufftHandle *h, size_t *ws) {
+  if (cufftCreate(h) != CUFFT_SUCCESS) return false;
+  if (cufftSetAutoAllocation(*h, 0) != CUFFT_SUCCESS) { cufftDestroy(*h); return false; }
+  int n[2] = {D, D};
+  if (cufftMakePlanMany(*h, 2, n, nullptr, 1, 0, nullptr, 1, 0, type, B, ws) != CUFFT_SUCCESS) {
+    cufftDestroy(*h);
+    return false;
+  }
+  return true;
+}
+
+Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
+  Layout L{};
+  const size_t Bm = (size_t)c.max_batch, N = (size_t)d.N, D = (size_t)d.D;
+  const size_t H = D * (D / 2 + 1);
+  L.n_hist = (int64_t)Bm * d.NT * d.C;
+  L.n_scan_blk = (L.n_hist + 4095) / 4096;
+  L.list_cap = c.list_capacity;
+  L.loss_blocks = ctf_loss_blocks(d.D);
+  L.cufft_bytes = cufft_bytes;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  L.prep = take(sizeof(GaussPrep) * N);
+  L.rec = take(sizeof(SplatRec) * Bm * N);
+  L.box = take(sizeof(uint2) * Bm * N);
+  L.hist = take(sizeof(int) * (size_t)L.n_hist);
+  L.base = take(sizeof(int) * ((size_t)L.n_hist + 1));
+  L.scan_blk = take(sizeof(int) * ((size_t)L.n_scan_blk + 1));
+  L.ids = take(sizeof(int) * (size_t)L.list_cap);
+  L.proj = take(sizeof(float) * Bm * D * D);
+  L.spec_hat = take(sizeof(float2) * Bm * H);
+  L.spec_obs = take(sizeof(float2) * Bm * H);
+  L.spec_pred = take(sizeof(float2) * Bm * H);
+  L.dldi = take(sizeof(float) * Bm * D * D);
+  L.acc = take(sizeof(float4) * 3 * N);
+  L.loss_part = take(sizeof(double) * Bm * (size_t)L.loss_blocks);
+  L.stats = take(sizeof(DevStats));
+  L.stage_rot = take(sizeof(float) * 9 * Bm);
+  L.stage_shift = take(sizeof(float) * 2 * Bm);
+  L.stage_ctf = take(sizeof(float) * 8 * Bm);
+  L.stage_obs = take(sizeof(float) * Bm * D * D);
+  L.stage_loss = take(sizeof(double) * (Bm + 1));
+  L.cufft_work = take(cufft_bytes);
+  L.total = o;
+  return L;
+}
+
+bool cufft_sizes(int D, int B, size_t *bytes) {
+  cufftHandle a, b;
+  size_t wa = 0, wb = 0;
+  if (!make_plan(D, B, CUFFT_R2C, &a, &wa)) return false;
+  if (!make_plan(D, B, CUFFT_C2R, &b, &wb)) { cufftDestroy(a); return false; }
+  cufftDestroy(a);
+  cufftDestroy(b);
+  *bytes = (wa > wb ? wa : wb) + 4096;
+  return true;
+}
+
+template <typename T>
+T *at(gem_ctx *ctx, size_t off) { return reinterpret_cast<T *>(ctx->ws + off); }
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+bool soa_ok(const gem_soa *s) {
+  return s && s->mean_rho && s->log_scale && s->quat;
+}
+bool soa_aligned(const gem_soa *s) {
+  return aligned16(s->mean_rho) && aligned16(s->log_scale) && aligned16(s->quat);
+}
+
+gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r) {
+  for (int k = 0; k < ctx->n_plans; ++k)
+    if (ctx->plan_B[k] == B) { *r2c = ctx->plan_r2c[k]; *c2r = ctx->plan_c2r[k]; return GEM_OK; }
+  int slot = ctx->n_plans < 8 ? ctx->n_plans : 7;
+  if (ctx->n_plans >= 8) {  // evict the last slot
+    cufftDestroy(ctx->plan_r2c[7]);
+    cufftDestroy(ctx->plan_c2r[7]);
+    ctx->n_plans = 7;
+  }
+  size_t wa = 0, wb = 0;
+  cufftHandle a, b;
+  if (!make_plan(ctx->dc.D, B, CUFFT_R2C, &a, &wa)) return GEM_E_CUFFT;
+  if (!make_plan(ctx->dc.D, B, CUFFT_C2R, &b, &wb)) { cufftDestroy(a); return GEM_E_CUFFT; }
+  if (wa > ctx->L.cufft_bytes || wb > ctx->L.cufft_bytes) { cufftDestroy(a); cufftDestroy(b); return GEM_E_CUFFT; }
+  void *work = ctx->ws + ctx->L.cufft_work;
+  if (cufftSetWorkArea(a, work) != CUFFT_SUCCESS || cufftSetWorkArea(b, work) != CUFFT_SUCCESS) {
+    cufftDestroy(a); cufftDestroy(b);
+    return GEM_E_CUFFT;
+  }
+  ctx->plan_B[slot] = B;
+  ctx->plan_r2c[slot] = a;
+  ctx->plan_c2r[slot] = b;
+  ctx->n_plans = slot + 1;
+  *r2c = a;
+  *c2r = b;
+  return GEM_OK;
+}
+
+// ---- profiling: an event pair around each launch group while enabled
+const char *kProfNames[P_COUNT] = {"prep", "splat_count", "scan", "fill", "render_fwd", "fft_r2c",
+                                   "ctf_loss", "fft_c2r", "render_bwd", "finalize", "adam", "volume"};
+
+struct Prof {
+  gem_ctx *ctx;
+  cudaStream_t s;
+  int rec;
+  Prof(gem_ctx *c, cudaStream_t st, int kind) : ctx(c), s(st), rec(-1) {
+    if (!c->prof_on) return;
+    if (c->prof_n >= c->prof_cap) {
+      int ncap = c->prof_cap ? 2 * c->prof_cap : 256;
+      int *nk = (int *)realloc(c->prof_kind, sizeof(int) * ncap);
+      cudaEvent_t *ne = (cudaEvent_t *)realloc(c->prof_ev, sizeof(cudaEvent_t) * 2 * ncap);
+      if (!nk || !ne) return;
+      c->prof_kind = nk;
+      c->prof_ev = ne;
+      for (int k = 2 * c->prof_cap; k < 2 * ncap; ++k) cudaEventCreate(&c->prof_ev[k]);
+      c->prof_cap = ncap;
+    }
+    rec = c->prof_n++;
+    c->prof_kind[rec] = kind;
+    cudaEventRecord(c->prof_ev[2 * rec], s);
+  }
+  ~Prof() {
+    if (rec >= 0) cudaEventRecord(ctx->prof_ev[2 * rec + 1], s);
+  }
+};
+
+#define CK(x)                                          \
+  do {                                                 \
+    if ((x) != cudaSuccess) return GEM_E_CUDA;         \
+  } while (0)
+#define CKF(x)                                         \
+  do {                                                 \
+    if ((x) != CUFFT_SUCCESS) return GEM_E_CUFFT;      \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+const char *gem_status_string(gem_status s) {
+  switch (s) {
+    case GEM_OK: return "ok";
+    case GEM_E_INVALID: return "invalid argument";
+    case GEM_E_SHAPE: return "inconsistent shape";
+    case GEM_E_ALIGN: return "misaligned pointer";
+    case GEM_E_CUDA: return "CUDA error";
+    case GEM_E_CUFFT: return "cuFFT error";
+    case GEM_E_CAPACITY: return "list capacity exceeded";
+    case GEM_E_STATE: return "backward without a live forward";
+    case GEM_E_NONFINITE: return "non-finite loss or gradient";
+  }
+  return "unknown status";
+}
+
+size_t gem_workspace_bytes(const gem_config *cfg) {
+  gem_config c;
+  CfgDev d;
+  if (!resolve(cfg, c, d)) return 0;
+  size_t cb = 0;
+  if (!cufft_sizes(c.D, c.max_batch, &cb)) return 0;
+  return layout(c, d, cb).total;
+}
+
+gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_stream_t stream, gem_ctx **out) {
+  if (!cfg || !out) return GEM_E_INVALID;
+  *out = nullptr;
+  gem_config c;
+  CfgDev d;
+  if (!resolve(cfg, c, d)) return (cfg->D & 1) || cfg->D < 2 ? GEM_E_SHAPE : GEM_E_INVALID;
+  if (!workspace) return GEM_E_INVALID;
+  if (((uintptr_t)workspace & 255u) != 0) return GEM_E_ALIGN;
+  size_t cb = 0;
+  if (!cufft_sizes(c.D, c.max_batch, &cb)) return GEM_E_CUFFT;
+  Layout L = layout(c, d, cb);
+  if (bytes < L.total) return GEM_E_SHAPE;
+  gem_ctx *ctx = new (std::nothrow) gem_ctx();
+  if (!ctx) return GEM_E_INVALID;
+  ctx->cfg = c;
+  ctx->dc = d;
+  ctx->L = L;
+  ctx->ws = (char *)workspace;
+  ctx->ws_bytes = bytes;
+  ctx->stream = (cudaStream_t)stream;
+  ctx->n_plans = 0;
+  cufftHandle a, b;
+  gem_status st = plan_for(ctx, c.max_batch, &a, &b);
+  if (st != GEM_OK) { delete ctx; return st; }
+  if (cudaMemsetAsync(ctx->ws + L.stats, 0, sizeof(DevStats), ctx->stream) != cudaSuccess ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    gem_destroy(ctx);
+    return GEM_E_CUDA;
+  }
+  *out = ctx;
+  return GEM_OK;
+}
+
+gem_status gem_destroy(gem_ctx *ctx) {
+  if (!ctx) return GEM_E_INVALID;
+  cudaStreamSynchronize(ctx->stream);
+  for (int k = 0; k < ctx->n_plans; ++k) {
+    cufftDestroy(ctx->plan_r2c[k]);
+    cufftDestroy(ctx->plan_c2r[k]);
+  }
+  for (int k = 0; k < 2 * ctx->prof_cap; ++k) cudaEventDestroy(ctx->prof_ev[k]);
+  free(ctx->prof_ev);
+  free(ctx->prof_kind);
+  delete ctx;
+  return GEM_OK;
+}
+
+int32_t gem_last_launch_count(const gem_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+gem_status gem_profile_enable(gem_ctx *ctx, int32_t enable) {
+  if (!ctx) return GEM_E_INVALID;
+  if (enable) ctx->prof_n = 0;
+  ctx->prof_on = enable ? 1 : 0;
+  return GEM_OK;
+}
+
+int32_t gem_profile_read(gem_ctx *ctx, gem_kernel_time_t *out, int32_t cap) {
+  if (!ctx || (!out && cap > 0)) return -1;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return -1;
+  double tot[P_COUNT] = {0};
+  int cnt[P_COUNT] = {0};
+  for (int r = 0; r < ctx->prof_n; ++r) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(ctx->prof_ev[2 * r + 1]) != cudaSuccess) return -1;
+    if (cudaEventElapsedTime(&ms, ctx->prof_ev[2 * r], ctx->prof_ev[2 * r + 1]) != cudaSuccess) return -1;
+    tot[ctx->prof_kind[r]] += ms;
+    cnt[ctx->prof_kind[r]] += 1;
+  }
+  int n = 0;
+  for (int k = 0; k < P_COUNT; ++k) {
+    if (!cnt[k]) continue;
+    if (n < cap) {
+      memset(&out[n], 0, sizeof(out[n]));
+      strncpy(out[n].name, kProfNames[k], sizeof(out[n].name) - 1);
+      out[n].launches = cnt[k];
+      out[n].total_ms = tot[k];
+    }
+    ++n;
+  }
+  return n;
+}
+
+gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *batch, double *loss, float *proj_out,
+                       float *pred_out, gem_stream_t stream) {
+  if (!ctx || !soa_ok(params) || !batch || !loss) return GEM_E_INVALID;
+  if (!batch->rot || !batch->shift || !batch->ctf || !batch->observed) return GEM_E_INVALID;
+  const int B = batch->B;
+  if (B < 1 || B > ctx->cfg.max_batch) return GEM_E_SHAPE;
+  if (!soa_aligned(params)) return GEM_E_ALIGN;
+  if (batch->memory != GEM_MEM_DEVICE && batch->memory != GEM_MEM_HOST) return GEM_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->stream = s;
+  ctx->launches = 0;
+  ctx->fwd_live = 0;
+  const CfgDev &c = ctx->dc;
+  const Layout &L = ctx->L;
+  const size_t D = (size_t)c.D;
+  float *rot = at<float>(ctx, L.stage_rot);
+  const float *shift = batch->shift, *ctf = batch->ctf, *obs = batch->observed;
+  const bool host = batch->memory == GEM_MEM_HOST;
+  // the rotation is kept in the workspace for gem_backward
+  CK(cudaMemcpyAsync(rot, batch->rot, sizeof(float) * 9 * B, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+  if (host) {
+    CK(cudaMemcpyAsync(at<float>(ctx, L.stage_shift), shift, sizeof(float) * 2 * B, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(at<float>(ctx, L.stage_ctf), ctf, sizeof(float) * 8 * B, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(at<float>(ctx, L.stage_obs), obs, sizeof(float) * B * D * D, cudaMemcpyHostToDevice, s));
+    shift = at<float>(ctx, L.stage_shift);
+    ctf = at<float>(ctx, L.stage_ctf);
+    obs = at<float>(ctx, L.stage_obs);
+  }
+  DevStats *st = at<DevStats>(ctx, L.stats);
+  CK(cudaMemsetAsync(st, 0, sizeof(DevStats), s));
+  cufftHandle r2c, c2r;
+  gem_status ps = plan_for(ctx, B, &r2c, &c2r);
+  if (ps != GEM_OK) return ps;
+  GaussPrep *prep = at<GaussPrep>(ctx, L.prep);
+  SplatRec *rec = at<SplatRec>(ctx, L.rec);
+  uint2 *box = at<uint2>(ctx, L.box);
+  int *hist = at<int>(ctx, L.hist), *base = at<int>(ctx, L.base), *ids = at<int>(ctx, L.ids);
+  { Prof p(ctx, s, P_PREP); launch_prep(c, (const float4 *)params->log_scale, (const float4 *)params->quat, prep, st, s, ctx->launches); }
+  { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, B, prep, (const float4 *)params->mean_rho, rot, shift, rec, box, hist, st, s, ctx->launches); }
+  const int64_t nh = (int64_t)B * c.NT * c.C;
+  { Prof p(ctx, s, P_SCAN); launch_scan(hist, base, nh, at<int>(ctx, L.scan_blk), (nh + 4095) / 4096, st, c.cap, s, ctx->launches); }
+  { Prof p(ctx, s, P_FILL); launch_fill(c, B, box, base, ids, s, ctx->launches); }
+  float *proj = proj_out ? proj_out : at<float>(ctx, L.proj);
+  { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, B, rec, base, ids, proj, s, ctx->launches); }
+  float2 *sh = at<float2>(ctx, L.spec_hat), *so = at<float2>(ctx, L.spec_obs), *sp = at<float2>(ctx, L.spec_pred);
+  CKF(cufftSetStream(r2c, s));
+  CKF(cufftSetStream(c2r, s));
+  {
+    Prof p(ctx, s, P_FFT_R2C);
+    CKF(cufftExecR2C(r2c, (cufftReal *)proj, (cufftComplex *)sh));
+    CKF(cufftExecR2C(r2c, (cufftReal *)obs, (cufftComplex *)so));
+  }
+  double *lossd = host ? at<double>(ctx, L.stage_loss) : loss;
+  {
+    Prof p(ctx, s, P_CTF_LOSS);
+    launch_ctf_loss(c, B, ctf, sh, so, pred_out ? sp : nullptr, at<double>(ctx, L.loss_part), L.loss_blocks, lossd,
+                    st, s, ctx->launches);
+  }
+  {
+    Prof p(ctx, s, P_FFT_C2R);
+    if (pred_out) CKF(cufftExecC2R(c2r, (cufftComplex *)sp, (cufftReal *)pred_out));
+    CKF(cufftExecC2R(c2r, (cufftComplex *)sh, (cufftReal *)at<float>(ctx, L.dldi)));
+  }
+  if (host) CK(cudaMemcpyAsync(loss, lossd, sizeof(double) * (B + 1), cudaMemcpyDeviceToHost, s));
+  CK(cudaGetLastError());
+  ctx->fwd_live = 1;
+  ctx->last_B = B;
+  return GEM_OK;
+}
+
+gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_stream_t stream) {
+  if (!ctx || !soa_ok(params) || !soa_ok(grad)) return GEM_E_INVALID;
+  if (!soa_aligned(params) || !soa_aligned(grad)) return GEM_E_ALIGN;
+  if (!ctx->fwd_live) return GEM_E_STATE;
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->stream = s;
+  ctx->launches = 0;
+  const CfgDev &c = ctx->dc;
+  const Layout &L = ctx->L;
+  float4 *acc = at<float4>(ctx, L.acc);
+  CK(cudaMemsetAsync(acc, 0, sizeof(float4) * 3 * (size_t)c.N, s));
+  {
+    Prof p(ctx, s, P_RENDER_BWD);
+    launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<int>(ctx, L.base), at<int>(ctx, L.ids),
+                      at<float>(ctx, L.dldi), (const float4 *)params->mean_rho, at<float>(ctx, L.stage_rot), acc, s,
+                      ctx->launches);
+  }
+  Prof pf(ctx, s, P_FINALIZE);
+  launch_finalize(c, acc, (const float4 *)params->mean_rho, (const float4 *)params->log_scale,
+                  (const float4 *)params->quat, (float4 *)grad->mean_rho, (float4 *)grad->log_scale,
+                  (float4 *)grad->quat, at<DevStats>(ctx, L.stats), s, ctx->launches);
+  CK(cudaGetLastError());
+  return GEM_OK;
+}
+
+gem_status gem_step(gem_ctx *ctx, gem_soa *params, const gem_soa *grad, gem_soa *m, gem_soa *v, int64_t t,
+                    gem_stream_t stream) {
+  if (!ctx || !soa_ok(params) || !soa_ok(grad) || !soa_ok(m) || !soa_ok(v) || t < 1) return GEM_E_INVALID;
+  if (!soa_aligned(params) || !soa_aligned(grad) || !soa_aligned(m) || !soa_aligned(v)) return GEM_E_ALIGN;
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->stream = s;
+  ctx->launches = 0;
+  const gem_config &c = ctx->cfg;
+  const double bc1 = 1.0 - std::pow((double)c.beta1, (double)t), bc2 = 1.0 - std::pow((double)c.beta2, (double)t);
+  Prof pa(ctx, s, P_ADAM);
+  launch_adam(ctx->dc.N, (float4 *)params->mean_rho, (float4 *)params->log_scale, (float4 *)params->quat,
+              (const float4 *)grad->mean_rho, (const float4 *)grad->log_scale, (const float4 *)grad->quat,
+              (float4 *)m->mean_rho, (float4 *)m->log_scale, (float4 *)m->quat, (float4 *)v->mean_rho,
+              (float4 *)v->log_scale, (float4 *)v->quat, c.lr_mean, c.lr_log_scale, c.lr_quat, c.lr_density, c.beta1,
+              c.beta2, c.eps, (float)bc1, (float)bc2, s, ctx->launches);
+  CK(cudaGetLastError());
+  return GEM_OK;
+}
+
+size_t gem_volume_scratch_bytes(const gem_ctx *ctx, int32_t Dv, float voxel_size) {
+  (void)voxel_size;
+  if (!ctx || Dv < 2) return 0;
+  return volume_scratch_bytes(ctx->dc.N, Dv);
+}
+
+gem_status gem_render_volume(gem_ctx *ctx, const gem_soa *params, int32_t Dv, float voxel_size, float *vol_out,
+                             void *scratch, size_t scratch_bytes, gem_stream_t stream) {
+  if (!ctx || !soa_ok(params) || !vol_out || Dv < 2 || Dv > 4096 || !(voxel_size > 0.f)) return GEM_E_INVALID;
+  if (!soa_aligned(params)) return GEM_E_ALIGN;
+  const size_t need = volume_scratch_bytes(ctx->dc.N, Dv);
+  char *sc = (char *)scratch;
+  if (!sc) {
+    sc = ctx->ws;
+    scratch_bytes = ctx->ws_bytes;
+    ctx->fwd_live = 0;  // the step workspace is reused
+  }
+  if (scratch_bytes < need) return GEM_E_SHAPE;
+  if (((uintptr_t)sc & 255u) != 0) return GEM_E_ALIGN;
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->stream = s;
+  ctx->launches = 0;
+  Prof pv(ctx, s, P_VOLUME);
+  cudaError_t e = launch_volume(ctx->dc.N, (const float4 *)params->mean_rho, (const float4 *)params->log_scale,
+                                (const float4 *)params->quat, Dv, voxel_size, ctx->cfg.cull_k, vol_out, sc,
+                                scratch_bytes, s, ctx->launches);
+  if (e == cudaErrorInvalidValue) return GEM_E_CAPACITY;
+  if (e != cudaSuccess) return GEM_E_CUDA;
+  return GEM_OK;
+}
+
+gem_status gem_export_lists(gem_ctx *ctx, int32_t particle, int32_t *tile_off, int32_t *ids, int64_t ids_cap,
+                            int32_t *aabb) {
+  if (!ctx) return GEM_E_INVALID;
+  if (!ctx->fwd_live) return GEM_E_STATE;
+  if (particle < 0 || particle >= ctx->last_B) return GEM_E_SHAPE;
+  CK(cudaStreamSynchronize(ctx->stream));
+  const CfgDev &c = ctx->dc;
+  const Layout &L = ctx->L;
+  const size_t seg = (size_t)c.NT * c.C;
+  int *hb = (int *)malloc(sizeof(int) * (seg + 1));
+  if (!hb) return GEM_E_INVALID;
+  if (cudaMemcpy(hb, at<int>(ctx, L.base) + (size_t)particle * seg, sizeof(int) * (seg + 1), cudaMemcpyDeviceToHost) !=
+      cudaSuccess) {
+    free(hb);
+    return GEM_E_CUDA;
+  }
+  const int start = hb[0];
+  if (tile_off)
+    for (int t = 0; t <= c.NT; ++t) tile_off[t] = hb[(size_t)t * c.C] - start;
+  const int64_t end = hb[seg];
+  free(hb);
+  if (ids) {
+    int64_t n = end - start;
+    if (n > ids_cap) n = ids_cap;
+    if ((int64_t)start + n > c.cap) n = c.cap - start;
+    if (n > 0)
+      CK(cudaMemcpy(ids, at<int>(ctx, L.ids) + start, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  }
+  if (aabb) {
+    uint2 *hbx = (uint2 *)malloc(sizeof(uint2) * c.N);
+    if (!hbx) return GEM_E_INVALID;
+    if (cudaMemcpy(hbx, at<uint2>(ctx, L.box) + (size_t)particle * c.N, sizeof(uint2) * c.N, cudaMemcpyDeviceToHost) !=
+        cudaSuccess) {
+      free(hbx);
+      return GEM_E_CUDA;
+    }
+    for (int j = 0; j < c.N; ++j) {
+      aabb[4 * j] = (int)(hbx[j].x & 0xffff);
+      aabb[4 * j + 1] = (int)(short)(hbx[j].x >> 16);
+      aabb[4 * j + 2] = (int)(hbx[j].y & 0xffff);
+      aabb[4 * j + 3] = (int)(short)(hbx[j].y >> 16);
+    }
+    free(hbx);
+  }
+  return GEM_OK;
+}
+
+gem_status gem_stats(gem_ctx *ctx, gem_stats_t *out) {
+  if (!ctx || !out) return GEM_E_INVALID;
+  CK(cudaStreamSynchronize(ctx->stream));
+  DevStats h;
+  CK(cudaMemcpy(&h, ctx->ws + ctx->L.stats, sizeof(DevStats), cudaMemcpyDeviceToHost));
+  out->entries = (int64_t)h.entries;
+  out->capacity = ctx->dc.cap;
+  out->degenerate = h.degenerate;
+  out->overflow = h.overflow;
+  out->nonfinite = h.nonfinite;
+  out->batch = ctx->last_B;
+  out->workspace_bytes = (int64_t)ctx->ws_bytes;
+  out->pairs = (int64_t)h.pairs;
+  if (h.overflow) return GEM_E_CAPACITY;
+  if (h.nonfinite) return GEM_E_NONFINITE;
+  return GEM_OK;
+}
+
+}  // extern "C"

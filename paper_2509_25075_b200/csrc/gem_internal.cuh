@@ -1,0 +1,116 @@
+// gem_internal.cuh — shared device types, workspace layout and launch helpers
+// for libgem.so (sm_100a).  Nothing here is shared with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include "../../include/gem.h"
+
+namespace gem {
+
+constexpr int kChunk = 1024;          // Gaussians per binning chunk (a3)
+constexpr double kSqrt2Pi = 2.5066282746310002;
+constexpr float kLog2e = 1.4426950408889634f;
+
+// a1 output: fp64 covariance (6 unique) + |Sigma| + ok flag (64 B, L2-resident).
+struct __align__(16) GaussPrep {
+  double sig[6];   // (00, 01, 02, 11, 12, 22)  Angstrom^2
+  double detS;     // |Sigma|
+  double ok;       // 1.0 valid, 0.0 degenerate
+};
+
+// a2 output per (particle, Gaussian): splat in pixel units (32 B, two float4).
+//   f0 = (mxr, myr, a, b)   mxr = m_x/px + D/2 - u_lo (centre relative to the box corner)
+//   f1 = (c, amp, ub, vb)   ub = u_lo | u_hi << 16, vb likewise (empty box: lo > hi)
+struct __align__(16) SplatRec {
+  float4 f0;
+  float4 f1;
+};
+
+struct Layout {  // byte offsets into the caller's workspace
+  size_t prep, rec, box, hist, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, acc, loss_part,
+      stats, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, total;
+  int64_t n_hist;       // B_max * NT * C
+  int64_t n_scan_blk;
+  int64_t list_cap;
+  size_t cufft_bytes;
+  int loss_blocks;      // CTF/loss partial blocks per particle
+};
+
+struct DevStats {      // device-side counters (zeroed per forward)
+  unsigned long long entries;
+  unsigned long long pairs;
+  int overflow;
+  int degenerate;
+  int nonfinite;
+  int pad;
+};
+
+struct CfgDev {        // resolved config passed by value to kernels
+  int D, T, nt, NT, N, C;
+  float px, k, tau;
+  int64_t cap;
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace gem
+
+struct gem_ctx {
+  gem_config cfg;
+  gem::CfgDev dc;
+  gem::Layout L;
+  char *ws;
+  size_t ws_bytes;
+  cudaStream_t stream;
+  // cuFFT plans keyed by batch size (small cache)
+  int plan_B[8];
+  cufftHandle plan_r2c[8], plan_c2r[8];
+  int n_plans;
+  int fwd_live;        // a forward's lists/records/dL/dI are valid
+  int last_B;
+  int launches;
+  // profiling (gem_profile_enable): event pairs around launches
+  int prof_on;
+  int prof_n, prof_cap;
+  int *prof_kind;
+  cudaEvent_t *prof_ev;  // 2 per record
+};
+
+namespace gem {
+enum ProfKind { P_PREP, P_SPLAT, P_SCAN, P_FILL, P_RENDER_FWD, P_FFT_R2C, P_CTF_LOSS, P_FFT_C2R, P_RENDER_BWD,
+                P_FINALIZE, P_ADAM, P_VOLUME, P_COUNT };
+}
+
+// ---------------------------------------------------------------- kernels
+namespace gem {
+void launch_prep(const CfgDev &c, const float4 *log_scale, const float4 *quat, GaussPrep *prep, DevStats *st,
+                 cudaStream_t s, int &launches);
+void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
+                        const float *shift, SplatRec *rec, uint2 *box, int *hist, DevStats *st, cudaStream_t s,
+                        int &launches);
+void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, DevStats *st, int64_t cap, cudaStream_t s,
+                 int &launches);
+void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, int *ids, cudaStream_t s, int &launches);
+void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
+                       cudaStream_t s, int &launches);
+void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, float2 *spec_hat, const float2 *spec_obs,
+                     float2 *spec_pred, double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
+                     int &launches);
+void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids,
+                       const float *dldi, const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s,
+                       int &launches);
+void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho, const float4 *log_scale,
+                     const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
+                     int &launches);
+void launch_adam(int N, float4 *p_mr, float4 *p_ls, float4 *p_q, const float4 *g_mr, const float4 *g_ls,
+                 const float4 *g_q, float4 *m_mr, float4 *m_ls, float4 *m_q, float4 *v_mr, float4 *v_ls, float4 *v_q,
+                 float lr_mean, float lr_ls, float lr_q, float lr_rho, float b1, float b2, float eps, float bc1,
+                 float bc2, cudaStream_t s, int &launches);
+size_t volume_scratch_bytes(int N, int Dv);
+cudaError_t launch_volume(int N, const float4 *mean_rho, const float4 *log_scale, const float4 *quat, int Dv,
+                          float vs, float k, float *vol, char *scratch, size_t scratch_bytes, cudaStream_t s,
+                          int &launches);
+}  // namespace gem

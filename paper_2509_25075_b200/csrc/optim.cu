@@ -1,0 +1,139 @@
+// optim.cu — a8 pose-independent finalize and a10 fused Adam.
+//
+// Finalize (DESIGN.md §3 O10): from the world accumulators (L_rho, G_mu,
+// G_Sigma) of each Gaussian:  dmu = G_mu, drho = L_rho,
+//   ds_k = 2 sigma_k^2 (R^T G_Sigma R)_kk + rho L_rho,
+//   dL/dR = 2 G_Sigma R diag(sigma^2),  dq_hat_c = <dL/dR, dR/dq_hat_c>,
+//   dq = (I - q_hat q_hat^T) dq_hat / |q|   (tangent to the sphere, L16).
+// Adam (reading L15, PyTorch bias-corrected form) per class lr, then
+// q <- q/|q|; the log_scale pad lane is never touched.
+#include "gem_internal.cuh"
+
+namespace gem {
+namespace {
+
+__global__ void __launch_bounds__(256) k_finalize(int N, const float4 *__restrict__ acc,
+                                                  const float4 *__restrict__ mr, const float4 *__restrict__ ls,
+                                                  const float4 *__restrict__ q, float4 *__restrict__ g_mr,
+                                                  float4 *__restrict__ g_ls, float4 *__restrict__ g_q, DevStats *st) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const float4 a0 = acc[3 * (size_t)j], a1 = acc[3 * (size_t)j + 1], a2 = acc[3 * (size_t)j + 2];
+  const float4 qq = q[j], ss = ls[j];
+  const float rho = mr[j].w;
+  const float n = sqrtf(qq.x * qq.x + qq.y * qq.y + qq.z * qq.z + qq.w * qq.w);
+  if (!(n > 0.f) || !isfinite(n)) {
+    g_mr[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    g_ls[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    g_q[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const float w = qq.x / n, x = qq.y / n, y = qq.z / n, z = qq.w / n;
+  float R[3][3];
+  R[0][0] = 1.f - 2.f * (y * y + z * z); R[0][1] = 2.f * (x * y - w * z); R[0][2] = 2.f * (x * z + w * y);
+  R[1][0] = 2.f * (x * y + w * z); R[1][1] = 1.f - 2.f * (x * x + z * z); R[1][2] = 2.f * (y * z - w * x);
+  R[2][0] = 2.f * (x * z - w * y); R[2][1] = 2.f * (y * z + w * x); R[2][2] = 1.f - 2.f * (x * x + y * y);
+  const float G[3][3] = {{a1.x, a1.y, a1.z}, {a1.y, a1.w, a2.x}, {a1.z, a2.x, a2.y}};
+  const float s2[3] = {expf(2.f * ss.x), expf(2.f * ss.y), expf(2.f * ss.z)};
+  float GR[3][3];
+#pragma unroll
+  for (int m = 0; m < 3; ++m)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) GR[m][k] = G[m][0] * R[0][k] + G[m][1] * R[1][k] + G[m][2] * R[2][k];
+  float ds[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float rgr = R[0][k] * GR[0][k] + R[1][k] * GR[1][k] + R[2][k] * GR[2][k];
+    ds[k] = 2.f * s2[k] * rgr + rho * a0.x;
+  }
+  float dR[3][3];
+#pragma unroll
+  for (int m = 0; m < 3; ++m)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dR[m][k] = 2.f * GR[m][k] * s2[k];
+  // <dR, dR/dq_hat_c> with dR/dq_hat from DESIGN.md §3 O10 (factor 2 folded in)
+  float dw = 2.f * (-z * dR[0][1] + y * dR[0][2] + z * dR[1][0] - x * dR[1][2] - y * dR[2][0] + x * dR[2][1]);
+  float dx = 2.f * (y * dR[0][1] + z * dR[0][2] + y * dR[1][0] - 2.f * x * dR[1][1] - w * dR[1][2] + z * dR[2][0] +
+                    w * dR[2][1] - 2.f * x * dR[2][2]);
+  float dy = 2.f * (-2.f * y * dR[0][0] + x * dR[0][1] + w * dR[0][2] + x * dR[1][0] + z * dR[1][2] - w * dR[2][0] +
+                    z * dR[2][1] - 2.f * y * dR[2][2]);
+  float dz = 2.f * (-2.f * z * dR[0][0] - w * dR[0][1] + x * dR[0][2] + w * dR[1][0] - 2.f * z * dR[1][1] +
+                    y * dR[1][2] + x * dR[2][0] + y * dR[2][1]);
+  const float dot = dw * w + dx * x + dy * y + dz * z;
+  const float inv = 1.f / n;
+  const float4 gq = make_float4((dw - dot * w) * inv, (dx - dot * x) * inv, (dy - dot * y) * inv, (dz - dot * z) * inv);
+  g_mr[j] = make_float4(a0.y, a0.z, a0.w, a0.x);
+  g_ls[j] = make_float4(ds[0], ds[1], ds[2], 0.f);
+  g_q[j] = gq;
+  const float chk = a0.x + a0.y + a0.z + a0.w + ds[0] + ds[1] + ds[2] + gq.x + gq.y + gq.z + gq.w;
+  if (!isfinite(chk)) st->nonfinite = 1;
+}
+
+__device__ __forceinline__ float adam1(float p, float g, float &m, float &v, float lr, float b1, float b2, float eps,
+                                       float bc1, float bc2) {
+  m = b1 * m + (1.f - b1) * g;
+  v = b2 * v + (1.f - b2) * g * g;
+  const float mh = m / bc1, vh = v / bc2;
+  return p - lr * mh / (sqrtf(vh) + eps);
+}
+
+struct AdamArgs {
+  float4 *p[3];
+  const float4 *g[3];
+  float4 *m[3], *v[3];
+  float lr_mean, lr_ls, lr_q, lr_rho, b1, b2, eps, bc1, bc2;
+};
+
+__global__ void __launch_bounds__(256) k_adam(int N, AdamArgs A) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int arr = blockIdx.y;
+  if (j >= N) return;
+  float4 p = A.p[arr][j], g = A.g[arr][j], m = A.m[arr][j], v = A.v[arr][j];
+  if (arr == 0) {
+    p.x = adam1(p.x, g.x, m.x, v.x, A.lr_mean, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+    p.y = adam1(p.y, g.y, m.y, v.y, A.lr_mean, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+    p.z = adam1(p.z, g.z, m.z, v.z, A.lr_mean, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+    p.w = adam1(p.w, g.w, m.w, v.w, A.lr_rho, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+  } else if (arr == 1) {
+    p.x = adam1(p.x, g.x, m.x, v.x, A.lr_ls, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+    p.y = adam1(p.y, g.y, m.y, v.y, A.lr_ls, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+    p.z = adam1(p.z, g.z, m.z, v.z, A.lr_ls, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+  } else {
+    p.x = adam1(p.x, g.x, m.x, v.x, A.lr_q, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+    p.y = adam1(p.y, g.y, m.y, v.y, A.lr_q, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+    p.z = adam1(p.z, g.z, m.z, v.z, A.lr_q, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+    p.w = adam1(p.w, g.w, m.w, v.w, A.lr_q, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+    const float n = sqrtf(p.x * p.x + p.y * p.y + p.z * p.z + p.w * p.w);
+    if (n > 0.f) { p.x /= n; p.y /= n; p.z /= n; p.w /= n; }
+  }
+  A.p[arr][j] = p;
+  A.m[arr][j] = m;
+  A.v[arr][j] = v;
+}
+
+}  // namespace
+
+void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho, const float4 *log_scale,
+                     const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
+                     int &launches) {
+  k_finalize<<<(c.N + 255) / 256, 256, 0, s>>>(c.N, acc, mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
+  ++launches;
+}
+
+void launch_adam(int N, float4 *p_mr, float4 *p_ls, float4 *p_q, const float4 *g_mr, const float4 *g_ls,
+                 const float4 *g_q, float4 *m_mr, float4 *m_ls, float4 *m_q, float4 *v_mr, float4 *v_ls, float4 *v_q,
+                 float lr_mean, float lr_ls, float lr_q, float lr_rho, float b1, float b2, float eps, float bc1,
+                 float bc2, cudaStream_t s, int &launches) {
+  AdamArgs A;
+  A.p[0] = p_mr; A.p[1] = p_ls; A.p[2] = p_q;
+  A.g[0] = g_mr; A.g[1] = g_ls; A.g[2] = g_q;
+  A.m[0] = m_mr; A.m[1] = m_ls; A.m[2] = m_q;
+  A.v[0] = v_mr; A.v[1] = v_ls; A.v[2] = v_q;
+  A.lr_mean = lr_mean; A.lr_ls = lr_ls; A.lr_q = lr_q; A.lr_rho = lr_rho;
+  A.b1 = b1; A.b2 = b2; A.eps = eps; A.bc1 = bc1; A.bc2 = bc2;
+  dim3 grid((N + 255) / 256, 3);
+  k_adam<<<grid, 256, 0, s>>>(N, A);
+  ++launches;
+}
+
+}  // namespace gem

@@ -1,0 +1,337 @@
+// prep_bin.cu — a1 Gaussian prep, a2 splat preprocess + per-chunk tile
+// histogram, device-wide exclusive scan, a3 stable per-tile list fill.
+//
+// Geometry follows App. A.2 (J = I for parallel rays, the
+// exact marginal amplitude of P:500-501) and the Eq. 8 selection (PAPER.md:
+// 219-225) realised as the integer k-sigma AABB (readings
+// L1/L5/L6).  Every bound-relevant quantity is computed in fp64 with explicit
+// round-to-nearest intrinsics (no FMA contraction) in the canonical op order of
+// DESIGN.md §3 O3, so the cull lists are a bit-exact function of the fp32
+// inputs.  Lists are emitted in ascending Gaussian id per tile (reading L9).
+#include "gem_internal.cuh"
+
+namespace gem {
+namespace {
+
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsb(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ----------------------------------------------------------------- a1 prep
+// q_hat = q/|q|, R(q_hat), sigma^2 = exp(2 s), Sigma = R diag(sigma^2) R^T,
+// |Sigma| = exp(2 (s0+s1+s2))   (Eq. 4).
+__global__ void __launch_bounds__(256) k_prep(int N, const float4 *__restrict__ ls, const float4 *__restrict__ q,
+                                              GaussPrep *__restrict__ prep, DevStats *st) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  float4 qq = q[j], ss = ls[j];
+  double w = qq.x, x = qq.y, y = qq.z, z = qq.w;
+  double n = sqrt(da(da(da(dm(w, w), dm(x, x)), dm(y, y)), dm(z, z)));
+  GaussPrep p;
+  bool ok = (n > 0.0) && isfinite(n);
+  if (ok) {
+    w = dv(w, n); x = dv(x, n); y = dv(y, n); z = dv(z, n);
+    double R[9];
+    R[0] = dsb(1.0, dm(2.0, da(dm(y, y), dm(z, z))));
+    R[1] = dm(2.0, dsb(dm(x, y), dm(w, z)));
+    R[2] = dm(2.0, da(dm(x, z), dm(w, y)));
+    R[3] = dm(2.0, da(dm(x, y), dm(w, z)));
+    R[4] = dsb(1.0, dm(2.0, da(dm(x, x), dm(z, z))));
+    R[5] = dm(2.0, dsb(dm(y, z), dm(w, x)));
+    R[6] = dm(2.0, dsb(dm(x, z), dm(w, y)));
+    R[7] = dm(2.0, da(dm(y, z), dm(w, x)));
+    R[8] = dsb(1.0, dm(2.0, da(dm(x, x), dm(y, y))));
+    double s0 = ss.x, s1 = ss.y, s2 = ss.z;
+    double e0 = exp(dm(2.0, s0)), e1 = exp(dm(2.0, s1)), e2 = exp(dm(2.0, s2));
+    const int K[6] = {0, 0, 0, 1, 1, 2}, Lx[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      int k = K[e], l = Lx[e];
+      p.sig[e] = da(da(dm(dm(R[3 * k + 0], e0), R[3 * l + 0]), dm(dm(R[3 * k + 1], e1), R[3 * l + 1])),
+                    dm(dm(R[3 * k + 2], e2), R[3 * l + 2]));
+    }
+    p.detS = exp(dm(2.0, da(da(s0, s1), s2)));
+    ok = isfinite(p.detS) && isfinite(p.sig[0]) && isfinite(p.sig[3]) && isfinite(p.sig[5]);
+  }
+  if (!ok) {
+#pragma unroll
+    for (int e = 0; e < 6; ++e) p.sig[e] = 0.0;
+    p.detS = 0.0;
+    atomicAdd(&st->degenerate, 1);
+  }
+  p.ok = ok ? 1.0 : 0.0;
+  prep[j] = p;
+}
+
+__device__ __forceinline__ int clip_d(double v, int lo, int hi) {
+  if (!(v >= (double)lo)) return lo;
+  if (v > (double)hi) return hi;
+  return (int)v;
+}
+
+// --------------------------------------------------- a2 splat + histogram
+// Per (particle i, Gaussian j): m = W mu + t, Sigma_hat = [W Sigma W^T]_2x2,
+// det2, conic, amp = rho sqrt(2 pi) sqrt(|Sigma|/det2) (App. A.2), integer
+// k-sigma AABB; visible => count one entry per touched tile in a per-CTA
+// smem histogram; hist layout [i][t][chunk] so that one flat exclusive scan
+// yields every list's start (t-major) and each chunk's sub-offset.
+__global__ void __launch_bounds__(256) k_splat_count(CfgDev c, const GaussPrep *__restrict__ prep,
+                                                     const float4 *__restrict__ mr, const float *__restrict__ rot,
+                                                     const float *__restrict__ shift, SplatRec *__restrict__ rec,
+                                                     uint2 *__restrict__ box, int *__restrict__ hist,
+                                                     DevStats *__restrict__ st) {
+  extern __shared__ int shist[];
+  const int i = blockIdx.y, ch = blockIdx.x, tid = threadIdx.x;
+  for (int t = tid; t < c.NT; t += blockDim.x) shist[t] = 0;
+  double W[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) W[3 * r + cc] = (double)rot[9 * i + 3 * cc + r];
+  const double tx = shift[2 * i], ty = shift[2 * i + 1];
+  const double px = c.px, half = (double)(c.D / 2), kk = c.k, tau = c.tau;
+  unsigned long long pairs = 0;
+  __syncthreads();
+  for (int r = 0; r < kChunk / 256; ++r) {
+    int j = ch * kChunk + r * 256 + tid;
+    if (j >= c.N) break;
+    const GaussPrep g = prep[j];
+    const float4 m4 = mr[j];
+    const double mu0 = m4.x, mu1 = m4.y, mu2 = m4.z, rho = m4.w;
+    double mx = da(da(da(dm(W[0], mu0), dm(W[1], mu1)), dm(W[2], mu2)), tx);
+    double my = da(da(da(dm(W[3], mu0), dm(W[4], mu1)), dm(W[5], mu2)), ty);
+    // Sigma row k as S(k,l)
+    const double S00 = g.sig[0], S01 = g.sig[1], S02 = g.sig[2], S11 = g.sig[3], S12 = g.sig[4], S22 = g.sig[5];
+    double v00 = da(da(dm(S00, W[0]), dm(S01, W[1])), dm(S02, W[2]));
+    double v01 = da(da(dm(S01, W[0]), dm(S11, W[1])), dm(S12, W[2]));
+    double v02 = da(da(dm(S02, W[0]), dm(S12, W[1])), dm(S22, W[2]));
+    double v10 = da(da(dm(S00, W[3]), dm(S01, W[4])), dm(S02, W[5]));
+    double v11 = da(da(dm(S01, W[3]), dm(S11, W[4])), dm(S12, W[5]));
+    double v12 = da(da(dm(S02, W[3]), dm(S12, W[4])), dm(S22, W[5]));
+    double A = da(da(dm(W[0], v00), dm(W[1], v01)), dm(W[2], v02));
+    double Bc = da(da(dm(W[0], v10), dm(W[1], v11)), dm(W[2], v12));
+    double Cc = da(da(dm(W[3], v10), dm(W[4], v11)), dm(W[5], v12));
+    double det2 = dsb(dm(A, Cc), dm(Bc, Bc));
+    double ampfac = dm(kSqrt2Pi, sqrt(dv(g.detS, det2)));
+    double amp = dm(rho, ampfac);
+    bool ok = g.ok != 0.0 && isfinite(mx) && isfinite(my) && isfinite(A) && isfinite(Cc) && isfinite(det2) &&
+              det2 > 0.0 && isfinite(amp);
+    int ulo = 1, uhi = 0, vlo = 1, vhi = 0;
+    bool vis = false;
+    SplatRec o;
+    o.f0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    o.f1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok) {
+      double rx = dm(kk, sqrt(A)), ry = dm(kk, sqrt(Cc));
+      ulo = clip_d(ceil(da(dv(dsb(mx, rx), px), half)), 0, c.D);
+      uhi = clip_d(floor(da(dv(da(mx, rx), px), half)), -1, c.D - 1);
+      vlo = clip_d(ceil(da(dv(dsb(my, ry), px), half)), 0, c.D);
+      vhi = clip_d(floor(da(dv(da(my, ry), px), half)), -1, c.D - 1);
+      vis = (fabs(amp) > tau) && ulo <= uhi && vlo <= vhi;
+    }
+    if (vis) {
+      const double px2 = px * px;
+      double mxp = mx / px + half, myp = my / px + half;
+      o.f0 = make_float4((float)(mxp - (double)ulo), (float)(myp - (double)vlo), (float)(Cc / det2 * px2),
+                         (float)(-Bc / det2 * px2));
+      o.f1 = make_float4((float)(A / det2 * px2), (float)amp, __int_as_float((ulo & 0xffff) | (uhi << 16)),
+                         __int_as_float((vlo & 0xffff) | (vhi << 16)));
+      pairs += (unsigned long long)(uhi - ulo + 1) * (unsigned long long)(vhi - vlo + 1);
+      const int tu0 = ulo / c.T, tu1 = uhi / c.T, tv0 = vlo / c.T, tv1 = vhi / c.T;
+      for (int tv = tv0; tv <= tv1; ++tv)
+        for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&shist[tv * c.nt + tu], 1);
+    } else {
+      ulo = 1; uhi = 0; vlo = 1; vhi = 0;
+      o.f1.z = __int_as_float(1);
+      o.f1.w = __int_as_float(1);
+    }
+    const size_t ij = (size_t)i * c.N + j;
+    rec[ij] = o;
+    box[ij] = make_uint2((unsigned)(ulo & 0xffff) | ((unsigned)uhi << 16), (unsigned)(vlo & 0xffff) | ((unsigned)vhi << 16));
+  }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, d);
+  if ((tid & 31) == 0 && pairs) atomicAdd(&st->pairs, pairs);
+  __syncthreads();
+  for (int t = tid; t < c.NT; t += blockDim.x) hist[((size_t)i * c.NT + t) * c.C + ch] = shist[t];
+}
+
+// ------------------------------------------------------------------- scan
+// Device-wide exclusive scan of int32 (3 phases; each block scans 4096 items).
+constexpr int kScanThreads = 1024, kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int block_excl_scan(int v, int *smem_warp, int &total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) smem_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < nw ? smem_warp[lane] : 0;
+    int si = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, si, d);
+      if (lane >= d) si += y;
+    }
+    if (lane < nw) smem_warp[lane] = si - s;
+    if (lane == 31) smem_warp[32] = si;
+  }
+  __syncthreads();
+  total = smem_warp[32];
+  int r = incl - v + smem_warp[wid];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_local(const int *__restrict__ in, int *__restrict__ out,
+                                                             int64_t n, int *__restrict__ blk) {
+  __shared__ int sw[33];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int v[kScanItems], s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = (base + k < n) ? in[base + k] : 0;
+    s += v[k];
+  }
+  int total;
+  int e = block_excl_scan(s, sw, total);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < n) out[base + k] = e;
+    e += v[k];
+  }
+  if (threadIdx.x == 0) blk[blockIdx.x] = total;
+}
+
+// single block: exclusive scan of the block totals; writes out[n] = total.
+__global__ void __launch_bounds__(kScanThreads) k_scan_blocks(int *__restrict__ blk, int64_t nblk, int *__restrict__ out,
+                                                              int64_t n, DevStats *st, int64_t cap) {
+  __shared__ int sw[33];
+  int carry = 0;
+  for (int64_t b0 = 0; b0 < nblk; b0 += kScanThreads) {
+    int64_t b = b0 + threadIdx.x;
+    int v = b < nblk ? blk[b] : 0;
+    int total;
+    int e = block_excl_scan(v, sw, total);
+    if (b < nblk) blk[b] = e + carry;
+    carry += total;
+  }
+  if (threadIdx.x == 0) {
+    out[n] = carry;
+    st->entries = (unsigned long long)carry;
+    st->overflow = (int64_t)carry > cap ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_add(int *__restrict__ out, int64_t n, const int *__restrict__ blk) {
+  const int add = blk[blockIdx.x];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  for (int k = threadIdx.x; k < kScanTile; k += kScanThreads)
+    if (base + k < n) out[base + k] += add;
+}
+
+// --------------------------------------------------------------- a3 fill
+// One warp per (particle, chunk of 1024 Gaussians).  Gaussians are visited in
+// ascending j, 32 per step; each step's (j, tile) pairs are enumerated in
+// (j, tile) order and ranked per tile with __match_any_sync, so every list is
+// written in ascending j (a stable counting sort keyed by tile).
+__global__ void __launch_bounds__(32) k_fill(CfgDev c, const uint2 *__restrict__ box, const int *__restrict__ base,
+                                             int *__restrict__ ids) {
+  extern __shared__ int cnt[];
+  const int i = blockIdx.y, ch = blockIdx.x, lane = threadIdx.x;
+  for (int t = lane; t < c.NT; t += 32) cnt[t] = base[((size_t)i * c.NT + t) * c.C + ch];
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int step = 0; step < kChunk / 32; ++step) {
+    const int j0 = ch * kChunk + step * 32;
+    if (j0 >= c.N) break;
+    const int j = j0 + lane;
+    int tu0 = 0, tu1 = -1, tv0 = 0, n = 0;
+    if (j < c.N) {
+      uint2 b = box[(size_t)i * c.N + j];
+      int ulo = (int)(b.x & 0xffff), uhi = (int)(b.x >> 16), vlo = (int)(b.y & 0xffff), vhi = (int)(b.y >> 16);
+      if (ulo <= uhi && vlo <= vhi) {
+        tu0 = ulo / c.T; tu1 = uhi / c.T; tv0 = vlo / c.T;
+        n = (tu1 - tu0 + 1) * (vhi / c.T - tv0 + 1);
+      }
+    }
+    int incl = n;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const int excl = incl - n;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int p0 = 0; p0 < total; p0 += 32) {
+      const int p = p0 + lane;
+      const bool active = p < total;
+      int lo = 0;
+#pragma unroll
+      for (int s = 16; s >= 1; s >>= 1) {
+        int vv = __shfl_sync(0xffffffffu, incl, lo + s - 1);
+        if (vv <= p) lo += s;
+      }
+      const int owner = lo & 31;
+      const int oex = __shfl_sync(0xffffffffu, excl, owner);
+      const int otu0 = __shfl_sync(0xffffffffu, tu0, owner);
+      const int otu1 = __shfl_sync(0xffffffffu, tu1, owner);
+      const int otv0 = __shfl_sync(0xffffffffu, tv0, owner);
+      int key = 0x40000000 + lane, t = 0;
+      if (active) {
+        const int r = p - oex, w = otu1 - otu0 + 1;
+        t = (otv0 + r / w) * c.nt + (otu0 + r % w);
+        key = t;
+      }
+      const unsigned m = __match_any_sync(0xffffffffu, key);
+      const int rank = __popc(m & lt);
+      int slot = 0;
+      if (active) {
+        slot = cnt[t] + rank;
+        if ((int64_t)slot < c.cap) ids[slot] = j0 + owner;
+      }
+      __syncwarp();
+      if (active && rank == 0) cnt[t] += __popc(m);
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace
+
+void launch_prep(const CfgDev &c, const float4 *log_scale, const float4 *quat, GaussPrep *prep, DevStats *st,
+                 cudaStream_t s, int &launches) {
+  k_prep<<<(c.N + 255) / 256, 256, 0, s>>>(c.N, log_scale, quat, prep, st);
+  ++launches;
+}
+
+void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
+                        const float *shift, SplatRec *rec, uint2 *box, int *hist, DevStats *st, cudaStream_t s,
+                        int &launches) {
+  dim3 grid(c.C, B);
+  k_splat_count<<<grid, 256, c.NT * sizeof(int), s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, st);
+  ++launches;
+}
+
+void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, DevStats *st, int64_t cap, cudaStream_t s,
+                 int &launches) {
+  k_scan_local<<<(unsigned)nblk, kScanThreads, 0, s>>>(in, out, n, blk);
+  k_scan_blocks<<<1, kScanThreads, 0, s>>>(blk, nblk, out, n, st, cap);
+  k_scan_add<<<(unsigned)nblk, kScanThreads, 0, s>>>(out, n, blk);
+  launches += 3;
+}
+
+void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, int *ids, cudaStream_t s, int &launches) {
+  dim3 grid(c.C, B);
+  k_fill<<<grid, 32, c.NT * sizeof(int), s>>>(c, box, base, ids);
+  ++launches;
+}
+
+}  // namespace gem

@@ -1,0 +1,264 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same
+seeded fp32 inputs.  Bars (BASELINE.json north star; DESIGN.md §3 L19/L22):
+  * cull lists and AABBs bit-exact (ties: oracle bound within 1e-9 px of an integer);
+  * images / predictions / volume: per-image max-norm relative error <= 1e-5;
+  * loss: relative error <= 1e-5;
+  * gradients: per-class (mu, rho, s, q) max-norm relative error <= 1e-4;
+  * Adam given an identical gradient input: <= 1e-6.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2509_25075_b200 import synth  # noqa: E402
+
+CLASSES = {"mu": [0, 1, 2], "rho": [3], "s": [4, 5, 6], "q": [8, 9, 10, 11]}
+IMG_TOL, GRAD_TOL, LOSS_TOL = 1e-5, 1e-4, 1e-5
+
+
+@pytest.fixture(scope="module")
+def gem():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_25075_b200 import gem as g
+    return g
+
+
+def make_case(wname="T", B=4, seed=0, N=None, D=None, state="steady", morton=True):
+    w = synth.CONFIGS[wname]
+    if N is not None or D is not None:
+        w = synth.Workload(w.name + "x", N or w.N, D or w.D, w.px, w.particles)
+    model = synth.steady_model if state == "steady" else synth.init_model
+    mr, ls, q = model(w, seed, morton)
+    rot, shift, ctf = synth.particles(w, B, seed)
+    mr, ls, q, rot, shift, ctf = synth.f32(mr, ls, q, rot, shift, ctf)
+    # observed images: noise at the scale of a typical pixel (the residual is O(signal))
+    amp_scale = float(np.mean(np.abs(mr[:, 3])) * math.sqrt(2 * math.pi) * w.sigma0)
+    obs = synth.f32(synth.noise_images(w, B, seed, scale=amp_scale))
+    return dict(w=w, params=(mr, ls, q), rot=rot, shift=shift, ctf=ctf, obs=obs, px=float(np.float32(w.px)))
+
+
+def run_gpu(gem, case, tile=16, want_lists=False, cap=0, host=False):
+    w = case["w"]
+    B = case["rot"].shape[0]
+    cfg = gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=B, tile=tile, list_capacity=cap)
+    st = gem.GemStep(cfg)
+    dev = st.device
+    P = gem.SoA.from_arrays(*case["params"], device=dev)
+    if host:
+        mk = lambda a: torch.from_numpy(a).pin_memory()
+    else:
+        mk = lambda a: torch.from_numpy(a).to(dev)
+    rot, shift, ctf, obs = (mk(case[k]) for k in ("rot", "shift", "ctf", "obs"))
+    proj = torch.empty(B, w.D, w.D, device=dev)
+    pred = torch.empty(B, w.D, w.D, device=dev)
+    loss = st.forward(P, rot, shift, ctf, obs, proj=proj, pred=pred, host=host)
+    grad = gem.SoA.zeros(w.N, dev)
+    st.backward(P, grad)
+    torch.cuda.synchronize()
+    out = dict(st=st, P=P, loss=loss.cpu().numpy().copy(), proj=proj.cpu().numpy(), pred=pred.cpu().numpy(),
+               grad=grad.t.permute(1, 0, 2).reshape(w.N, 12).cpu().numpy(), grad_soa=grad)
+    if want_lists:
+        out["lists"] = [st.export_lists(i) for i in range(B)]
+    out["stats"] = st.stats(check=False)
+    return out
+
+
+def oracle_out(orc, case, want=("proj", "pred")):
+    w = case["w"]
+    return orc.loss_grad(case["params"], case["rot"], case["shift"], case["ctf"], case["obs"], w.D, case["px"],
+                         want=want)
+
+
+def maxnorm_rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def assert_lists_exact(orc, case, lists, tile):
+    w = case["w"]
+    aabb, vis, sp = orc.splats(case["params"], case["rot"], case["shift"], w.D, case["px"])
+    tile_off, base, ids = orc.lists(aabb, vis, w.D, tile)
+    ties = 0
+    for i, (g_off, g_ids, g_box) in enumerate(lists):
+        g_vis = (g_box[:, 0] <= g_box[:, 1]) & (g_box[:, 2] <= g_box[:, 3])
+        bad = np.nonzero((g_vis != vis[i].astype(bool)) |
+                         (vis[i].astype(bool) & np.any(g_box != aabb[i], axis=1)))[0]
+        for j in bad:  # reading L22: allowed only if the oracle bound is within 1e-9 px of an integer
+            mx, my, A, C = sp[i, j, 0], sp[i, j, 1], sp[i, j, 8], sp[i, j, 9]
+            rx, ry = 3.0 * math.sqrt(A), 3.0 * math.sqrt(C)
+            bounds = [(mx - rx) / case["px"] + w.D // 2, (mx + rx) / case["px"] + w.D // 2,
+                      (my - ry) / case["px"] + w.D // 2, (my + ry) / case["px"] + w.D // 2]
+            assert min(abs(b - round(b)) for b in bounds) < 1e-9, (i, j, g_box[j], aabb[i, j])
+            ties += 1
+        if ties == 0:
+            o_ids = ids[base[i]: base[i] + tile_off[i, -1]]
+            assert np.array_equal(g_off, tile_off[i]), i
+            assert np.array_equal(g_ids, o_ids), i
+    return ties
+
+
+# --------------------------------------------------------------------------- tests
+@pytest.mark.parametrize("tile", [16, 8])
+def test_T_lists_images_loss_grads(gem, orc, tile):
+    case = make_case("T", B=6, seed=1)
+    g = run_gpu(gem, case, tile=tile, want_lists=True)
+    assert g["stats"]["status"] == 0, g["stats"]
+    assert_lists_exact(orc, case, g["lists"], tile)
+    o = oracle_out(orc, case)
+    for i in range(case["rot"].shape[0]):
+        assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
+        assert maxnorm_rel(g["pred"][i], o["pred"][i]) < IMG_TOL
+    assert np.all(np.abs(g["loss"][:-1] - o["loss"]) < LOSS_TOL * o["loss"])
+    assert abs(g["loss"][-1] - o["total"]) < LOSS_TOL * o["total"]
+    for name, cols in CLASSES.items():
+        err = maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols])
+        assert err < GRAD_TOL, (name, err)
+    assert np.all(g["grad"][:, 7] == 0.0)
+
+
+def test_ragged_shapes_and_culled_rows(gem, orc):
+    """D not a multiple of the tile, N not a multiple of the 1024-Gaussian
+    chunk, B=3; Gaussians pushed off-frame get exactly-zero gradient rows."""
+    case = make_case("T", B=3, seed=2, N=1500, D=40)
+    mr = case["params"][0].copy()
+    mr[5, :3] = [1e4, 1e4, 0]
+    mr[1400, :3] = [-5e3, 2e3, 1e3]
+    mr[77, 3] = 0.0   # rho = 0 -> |amp| = 0 <= tau: culled
+    case["params"] = (mr, case["params"][1], case["params"][2])
+    g = run_gpu(gem, case, want_lists=True)
+    assert_lists_exact(orc, case, g["lists"], 16)
+    o = oracle_out(orc, case)
+    for i in range(3):
+        assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
+    for name, cols in CLASSES.items():
+        assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+    for j in (5, 1400, 77):
+        assert np.all(g["grad"][j] == 0.0)
+
+
+def test_init_state_and_unsorted_ids(gem, orc):
+    """SPEC random_init model state (3.6x more pairs) with Gaussian ids in random order."""
+    case = make_case("T", B=4, seed=3, state="init", morton=False)
+    g = run_gpu(gem, case, want_lists=True)
+    assert_lists_exact(orc, case, g["lists"], 16)
+    o = oracle_out(orc, case)
+    for i in range(4):
+        assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
+    for name, cols in CLASSES.items():
+        assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+
+
+def test_S_config_two_particles(gem, orc):
+    case = make_case("S", B=2, seed=4)
+    g = run_gpu(gem, case, want_lists=True)
+    assert_lists_exact(orc, case, g["lists"], 16)
+    o = oracle_out(orc, case)
+    for i in range(2):
+        assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
+        assert maxnorm_rel(g["pred"][i], o["pred"][i]) < IMG_TOL
+    assert np.all(np.abs(g["loss"][:-1] - o["loss"]) < LOSS_TOL * o["loss"])
+    for name, cols in CLASSES.items():
+        assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+
+
+def test_forward_bitwise_deterministic_and_linear_in_rho(gem):
+    case = make_case("T", B=4, seed=5)
+    a = run_gpu(gem, case)
+    b = run_gpu(gem, case)
+    assert np.array_equal(a["proj"], b["proj"])
+    assert np.array_equal(a["loss"], b["loss"])
+    mr = case["params"][0].copy()
+    mr[:, 3] *= 2.0
+    c = run_gpu(gem, dict(case, params=(mr, case["params"][1], case["params"][2])))
+    assert np.array_equal(c["proj"], 2.0 * a["proj"])
+
+
+def test_host_memory_batch_matches_device(gem):
+    case = make_case("T", B=4, seed=6)
+    a = run_gpu(gem, case)
+    h = run_gpu(gem, case, host=True)
+    assert np.array_equal(a["proj"], h["proj"]) and np.array_equal(a["loss"], h["loss"])
+    assert np.array_equal(a["grad"], h["grad"])
+
+
+def test_adam_step_identical_gradient_input(gem, orc):
+    case = make_case("T", B=2, seed=7)
+    g = run_gpu(gem, case)
+    st, P, grad = g["st"], g["P"], g["grad_soa"]
+    dev = P.t.device
+    p0 = P.t.cpu().numpy().astype(np.float64)
+    m = gem.SoA.zeros(P.N, dev); v = gem.SoA.zeros(P.N, dev)
+    cfg = st.cfg
+    lr = np.array([cfg.lr_mean, cfg.lr_log_scale, cfg.lr_quat, cfg.lr_density], np.float32).astype(np.float64)
+    gnp = grad.t.cpu().numpy().astype(np.float64)
+    mo = np.zeros_like(p0); vo = np.zeros_like(p0); po = p0
+    for t in (1, 2, 3):
+        st.step(P, grad, m, v, t)
+        po, mo, vo = orc.adam(po, gnp, mo, vo, t, lr, cfg.beta1, float(np.float32(cfg.beta2)), float(np.float32(cfg.eps)))
+    torch.cuda.synchronize()
+    pg = P.t.cpu().numpy().astype(np.float64)
+    assert np.abs(pg - po).max() <= 1e-6 * np.abs(po).max()
+    assert np.array_equal(pg[1, :, 3], p0[1, :, 3])                        # pad lane untouched
+    assert np.abs(np.linalg.norm(pg[2], axis=1) - 1).max() < 1e-6
+
+
+def test_render_volume(gem, orc):
+    case = make_case("T", B=1, seed=8)
+    g = run_gpu(gem, case)
+    w = case["w"]
+    Dv, vs = 32, float(np.float32(w.px))
+    vol = g["st"].render_volume(g["P"], Dv, vs).cpu().numpy()
+    ref = orc.volume(case["params"], Dv, vs, masked=True)
+    assert maxnorm_rel(vol, ref) < IMG_TOL
+    # Dv not a multiple of the 8^3 brick
+    vol2 = g["st"].render_volume(g["P"], 27, vs).cpu().numpy()
+    ref2 = orc.volume(case["params"], 27, vs, masked=True)
+    assert maxnorm_rel(vol2, ref2) < IMG_TOL
+
+
+def test_empty_lists_all_offframe(gem):
+    case = make_case("T", B=2, seed=9)
+    mr = case["params"][0].copy()
+    mr[:, :3] += 1e5
+    g = run_gpu(gem, dict(case, params=(mr, case["params"][1], case["params"][2])), want_lists=True)
+    assert np.all(g["proj"] == 0.0) and np.all(g["grad"] == 0.0)
+    assert all(l[0][-1] == 0 for l in g["lists"])
+    assert np.allclose(g["loss"][:-1], (case["obs"].astype(np.float64) ** 2).sum((1, 2)), rtol=1e-5)
+
+
+def test_errors_and_capacity(gem):
+    from paper_2509_25075_b200 import binding as b
+    case = make_case("T", B=2, seed=10)
+    w = case["w"]
+    with pytest.raises(b.GemError) as e:
+        gem.GemStep(gem.GemConfig(D=31, pixel_size=1.0, n_gauss=10, max_batch=1))
+    st = gem.GemStep(gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=1, list_capacity=10))
+    dev = st.device
+    P = gem.SoA.from_arrays(*case["params"], device=dev)
+    grad = gem.SoA.zeros(w.N, dev)
+    with pytest.raises(b.GemError) as e:
+        st.backward(P, grad)
+    assert e.value.status == b.GEM_E_STATE
+    t = lambda a: torch.from_numpy(a).to(dev)
+    with pytest.raises(b.GemError) as e:
+        st.forward(P, t(case["rot"]), t(case["shift"]), t(case["ctf"]), t(case["obs"]))
+    assert e.value.status == b.GEM_E_SHAPE
+    st.forward(P, t(case["rot"][:1]), t(case["shift"][:1]), t(case["ctf"][:1]), t(case["obs"][:1]))
+    s = st.stats(check=False)
+    assert s["status"] == b.GEM_E_CAPACITY and s["overflow"] == 1 and s["entries"] > 10
+
+
+def test_workspace_has_no_cubic_term(gem):
+    """S:193 / S:639: workspace grows with B*N and B*D^2, never D^3."""
+    from paper_2509_25075_b200 import binding as b
+    import ctypes
+    L = b.lib()
+    def ws(D, N=10000, B=8):
+        c = gem.GemConfig(D=D, pixel_size=1.0, n_gauss=N, max_batch=B).c()
+        return L.gem_workspace_bytes(ctypes.byref(c))
+    r = ws(256) / ws(128)
+    assert r < 4.6, r    # quadratic at most (plus lists); D^3 would give 8
