@@ -149,7 +149,13 @@ def test_init_state_and_unsorted_ids(gem, orc):
     for i in range(4):
         assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
     for name, cols in CLASSES.items():
+        if name == "q":
+            continue
         assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+    # init-state Gaussians are isotropic, so dL/dq is identically zero (rotation does
+    # not change Sigma): the GPU's q-gradient must be fp32 noise next to the s-gradient.
+    assert np.abs(o["grad"][:, 8:12]).max() < 1e-12 * np.abs(o["grad"][:, 4:7]).max()
+    assert np.abs(g["grad"][:, 8:12]).max() < GRAD_TOL * np.abs(o["grad"][:, 4:7]).max()
 
 
 def test_S_config_two_particles(gem, orc):
@@ -182,7 +188,8 @@ def test_host_memory_batch_matches_device(gem):
     a = run_gpu(gem, case)
     h = run_gpu(gem, case, host=True)
     assert np.array_equal(a["proj"], h["proj"]) and np.array_equal(a["loss"], h["loss"])
-    assert np.array_equal(a["grad"], h["grad"])
+    # the backward accumulates with L2 vector atomics: order-dependent in the last bits only
+    assert np.abs(a["grad"] - h["grad"]).max() <= 1e-5 * np.abs(a["grad"]).max()
 
 
 def test_adam_step_identical_gradient_input(gem, orc):
