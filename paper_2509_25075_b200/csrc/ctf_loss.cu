@@ -5,7 +5,8 @@
 // [D][D/2+1]):  L_i = (1/D^2) sum_half w_k |R_k|^2  (w = 1 for k_x in {0, D/2},
 // else 2), and dL/dI_hat = C2R_unnormalised((2/D^2) C . R)  (C is real and
 // even; DESIGN.md §3 O7/O8).  The CTF (reading L10) is evaluated per bin with
-// the phase in fp64, reduced mod 2 pi, then fp32 sincos; Nyquist bins average
+// the phase in fp64 (it reaches ~420 rad at D=256), reduced mod 2 pi, then fp32
+// sincos on [-pi, pi]; Nyquist bins average
 // their +-1/(2 px) aliases (reading L12) so C(k) = C(-k) exactly.
 #include "gem_internal.cuh"
 
@@ -15,21 +16,25 @@ namespace {
 constexpr int kCtfThreads = 256;
 constexpr double kPi = 3.14159265358979323846;
 
+// Per-particle constants: chi(f) = K1s s^2 + K1d ast(f) - K2 s^4 + phi, with
+// s^2 = fx^2 + fy^2, ast = (fx^2 - fy^2) cos 2θ + 2 fx fy sin 2θ,
+// K1s = π λ (du + dv)/2, K1d = π λ (du - dv)/2, K2 = π Cs λ^3 / 2 — the CTFFIND
+// form of reading L10 with Δf s^2 expanded (no division by s^2).
 struct CtfP {
-  double du, dv, c2, s2a, lam, cs_A, alpha_s, alpha_c, phi, bfac;
+  double K1s, K1d, K2, c2, s2a, phi;
+  float alpha_s, alpha_c, bq;   // sqrt(1 - α^2), α, B/4
 };
 
 __device__ __forceinline__ float ctf_raw(const CtfP &p, double fx, double fy) {
-  const double s2 = fx * fx + fy * fy;
-  double df = 0.5 * (p.du + p.dv);
-  if (s2 > 0.0) df += 0.5 * (p.du - p.dv) * ((fx * fx - fy * fy) * p.c2 + 2.0 * fx * fy * p.s2a) / s2;
-  const double lam = p.lam;
-  double chi = kPi * lam * df * s2 - 0.5 * kPi * p.cs_A * lam * lam * lam * s2 * s2 + p.phi;
-  chi -= 2.0 * kPi * rint(chi / (2.0 * kPi));
+  const double fx2 = fx * fx, fy2 = fy * fy, s2 = fx2 + fy2;
+  const double ast = fma(fx2 - fy2, p.c2, 2.0 * fx * fy * p.s2a);
+  double chi = fma(s2, fma(-p.K2, s2, p.K1s), fma(p.K1d, ast, p.phi));
+  const double n = rint(chi * 0.15915494309189535);   // 1 / (2 pi)
+  chi = fma(-n, 6.283185307179586, chi);                // reduced to [-pi, pi]
   float sn, cs;
-  sincosf((float)chi, &sn, &cs);
-  const float env = expf((float)(-p.bfac * s2 * 0.25));
-  return -env * ((float)p.alpha_s * sn + (float)p.alpha_c * cs);
+  __sincosf((float)chi, &sn, &cs);                       // |abs err| < 4e-7 on [-pi, pi]
+  const float env = p.bq > 0.f ? __expf(-p.bq * (float)s2) : 1.f;
+  return -env * (p.alpha_s * sn + p.alpha_c * cs);
 }
 
 __global__ void __launch_bounds__(kCtfThreads) k_ctf_loss(CfgDev c, const float *__restrict__ ctf,
@@ -43,13 +48,18 @@ __global__ void __launch_bounds__(kCtfThreads) k_ctf_loss(CfgDev c, const float 
     const float *q = ctf + 8 * i;
     const double kV = q[3], V = kV * 1000.0;
     const double h = 6.62607015e-34, m0 = 9.1093837015e-31, e = 1.602176634e-19, cl = 299792458.0;
-    P.du = q[0]; P.dv = q[1];
-    P.c2 = cos(2.0 * (double)q[2]); P.s2a = sin(2.0 * (double)q[2]);
-    P.lam = h / sqrt(2.0 * m0 * e * V * (1.0 + e * V / (2.0 * m0 * cl * cl))) * 1e10;
-    P.cs_A = (double)q[4] * 1e7;
+    const double lam = h / sqrt(2.0 * m0 * e * V * (1.0 + e * V / (2.0 * m0 * cl * cl))) * 1e10;
+    const double du = q[0], dv = q[1];
+    P.K1s = kPi * lam * 0.5 * (du + dv);
+    P.K1d = kPi * lam * 0.5 * (du - dv);
+    P.K2 = 0.5 * kPi * ((double)q[4] * 1e7) * lam * lam * lam;
+    P.c2 = cos(2.0 * (double)q[2]);
+    P.s2a = sin(2.0 * (double)q[2]);
+    P.phi = q[6];
     const double al = q[5];
-    P.alpha_s = sqrt(1.0 - al * al); P.alpha_c = al;
-    P.phi = q[6]; P.bfac = q[7];
+    P.alpha_s = (float)sqrt(1.0 - al * al);
+    P.alpha_c = (float)al;
+    P.bq = 0.25f * q[7];
   }
   __syncthreads();
   const int D = c.D, Hx = D / 2 + 1;
@@ -58,12 +68,12 @@ __global__ void __launch_bounds__(kCtfThreads) k_ctf_loss(CfgDev c, const float 
   double lsum = 0.0;
   if (idx < H) {
     const int ky = idx / Hx, kx = idx - ky * Hx;
-    const double dpx = (double)D * (double)c.px, nyq = 1.0 / (2.0 * (double)c.px);
+    const double idpx = 1.0 / ((double)D * (double)c.px), nyq = 1.0 / (2.0 * (double)c.px);
     double fx[2], fy[2];
     int nx = 1, ny = 1;
-    if (2 * kx == D) { fx[0] = nyq; fx[1] = -nyq; nx = 2; } else fx[0] = kx / dpx;
+    if (2 * kx == D) { fx[0] = nyq; fx[1] = -nyq; nx = 2; } else fx[0] = kx * idpx;
     if (2 * ky == D) { fy[0] = nyq; fy[1] = -nyq; ny = 2; }
-    else fy[0] = (2 * ky < D ? ky : ky - D) / dpx;
+    else fy[0] = (2 * ky < D ? ky : ky - D) * idpx;
     float C = 0.f;
     for (int a = 0; a < nx; ++a)
       for (int b = 0; b < ny; ++b) C += ctf_raw(P, fx[a], fy[b]);
@@ -91,28 +101,28 @@ __global__ void __launch_bounds__(kCtfThreads) k_ctf_loss(CfgDev c, const float 
   }
 }
 
-// Deterministic reduction of the per-block partials: loss[i], then loss[B] = total.
-__global__ void k_loss_reduce(int B, int nblk, const double *__restrict__ part, double *__restrict__ loss, DevStats *st) {
-  __shared__ double li[1024];
-  double tot = 0.0;
-  for (int i0 = 0; i0 < B; i0 += blockDim.x) {
-    const int i = i0 + threadIdx.x;
-    if (i < B) {
-      double s = 0.0;
-      for (int b = 0; b < nblk; ++b) s += part[(size_t)i * nblk + b];
-      loss[i] = s;
-      li[threadIdx.x] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int m = min((int)blockDim.x, B - i0);
-      for (int k = 0; k < m; ++k) tot += li[k];
-    }
-    __syncthreads();
+// Deterministic reduction of the per-block partials: one warp per particle
+// (lane-strided sums, fixed xor tree), then warp 0 sums the particles in order.
+__global__ void __launch_bounds__(1024) k_loss_reduce(int B, int nblk, const double *__restrict__ part,
+                                                      double *__restrict__ loss, DevStats *st) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = w; i < B; i += nw) {
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += part[(size_t)i * nblk + b];
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+    if (lane == 0) loss[i] = s;
   }
-  if (threadIdx.x == 0) {
-    loss[B] = tot;
-    if (!isfinite(tot)) st->nonfinite = 1;
+  __syncthreads();
+  if (w == 0) {
+    double s = 0.0;
+    for (int i = lane; i < B; i += 32) s += loss[i];
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+    if (lane == 0) {
+      loss[B] = s;
+      if (!isfinite(s)) st->nonfinite = 1;
+    }
   }
 }
 

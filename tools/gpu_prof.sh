@@ -1,13 +1,16 @@
 #!/bin/bash
-# Profiling session: plain run, then launch list and ncu --set full of the render kernels.
+# Profiling session: plain run, then launch list and ncu --set full of selected kernels.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 TAG=${TAG:-r1}
+KREGEX=${KREGEX:-"k_render|k_fill|k_ctf_loss|k_splat"}
+SKIP=${SKIP:-32}
+COUNT=${COUNT:-5}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap --format=csv > gpurun_out/smi_query.txt 2>&1
 CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_render -s 4 -c 2 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"$KREGEX" -s $SKIP -c $COUNT -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "ncu rc=$?"
-tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/ncu_full_$TAG.log; ls -la gpurun_out
+tail -2 gpurun_out/ncu_full_$TAG.log; cat gpurun_out/smi_query.txt; ls -la gpurun_out
