@@ -14,11 +14,13 @@ constexpr int kChunk = 1024;          // Gaussians per binning chunk (a3)
 constexpr double kSqrt2Pi = 2.5066282746310002;
 constexpr float kLog2e = 1.4426950408889634f;
 
-// a1 output: fp64 covariance (6 unique) + |Sigma| + ok flag (64 B, L2-resident).
+// a1 output: fp64 covariance (6 unique) + |Sigma| + |Sigma|^1/2 + ok flag (80 B, L2-resident).
 struct __align__(16) GaussPrep {
   double sig[6];   // (00, 01, 02, 11, 12, 22)  Angstrom^2
   double detS;     // |Sigma|
+  double sdetS;    // |Sigma|^{1/2}
   double ok;       // 1.0 valid, 0.0 degenerate
+  double pad;
 };
 
 // a2 output per (particle, Gaussian): splat in pixel units (32 B, two float4).

@@ -52,12 +52,14 @@ __global__ void __launch_bounds__(256) k_prep(int N, const float4 *__restrict__ 
                     dm(dm(R[3 * k + 2], e2), R[3 * l + 2]));
     }
     p.detS = exp(dm(2.0, da(da(s0, s1), s2)));
+    p.sdetS = exp(da(da(s0, s1), s2));   // |Sigma|^{1/2} (amplitude only, not bound-critical)
     ok = isfinite(p.detS) && isfinite(p.sig[0]) && isfinite(p.sig[3]) && isfinite(p.sig[5]);
   }
   if (!ok) {
 #pragma unroll
     for (int e = 0; e < 6; ++e) p.sig[e] = 0.0;
     p.detS = 0.0;
+    p.sdetS = 0.0;
     atomicAdd(&st->degenerate, 1);
   }
   p.ok = ok ? 1.0 : 0.0;
@@ -90,7 +92,7 @@ __global__ void __launch_bounds__(256) k_splat_count(CfgDev c, const GaussPrep *
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) W[3 * r + cc] = (double)rot[9 * i + 3 * cc + r];
   const double tx = shift[2 * i], ty = shift[2 * i + 1];
-  const double px = c.px, half = (double)(c.D / 2), kk = c.k, tau = c.tau;
+  const double px = c.px, half = (double)(c.D / 2), kk = c.k, tau = c.tau, ipx = 1.0 / px;
   unsigned long long pairs = 0;
   __syncthreads();
   for (int r = 0; r < kChunk / 256; ++r) {
@@ -113,8 +115,12 @@ __global__ void __launch_bounds__(256) k_splat_count(CfgDev c, const GaussPrep *
     double Bc = da(da(dm(W[0], v10), dm(W[1], v11)), dm(W[2], v12));
     double Cc = da(da(dm(W[3], v10), dm(W[4], v11)), dm(W[5], v12));
     double det2 = dsb(dm(A, Cc), dm(Bc, Bc));
-    double ampfac = dm(kSqrt2Pi, sqrt(dv(g.detS, det2)));
-    double amp = dm(rho, ampfac);
+    // Fast path: bounds with a multiplication by 1/px (and rsqrt) instead of the
+    // canonical divisions; each floor/ceil is certain unless the fast value lies
+    // within 1e-9 px of an integer (fast vs canonical differ by ~1e-13 px), in
+    // which case the canonical O3 expression is evaluated exactly.
+    double ampfac = kSqrt2Pi * g.sdetS * rsqrt(det2);
+    double amp = rho * ampfac;
     bool ok = g.ok != 0.0 && isfinite(mx) && isfinite(my) && isfinite(A) && isfinite(Cc) && isfinite(det2) &&
               det2 > 0.0 && isfinite(amp);
     int ulo = 1, uhi = 0, vlo = 1, vhi = 0;
@@ -124,15 +130,31 @@ __global__ void __launch_bounds__(256) k_splat_count(CfgDev c, const GaussPrep *
     o.f1 = make_float4(0.f, 0.f, 0.f, 0.f);
     if (ok) {
       double rx = dm(kk, sqrt(A)), ry = dm(kk, sqrt(Cc));
-      ulo = clip_d(ceil(da(dv(dsb(mx, rx), px), half)), 0, c.D);
-      uhi = clip_d(floor(da(dv(da(mx, rx), px), half)), -1, c.D - 1);
-      vlo = clip_d(ceil(da(dv(dsb(my, ry), px), half)), 0, c.D);
-      vhi = clip_d(floor(da(dv(da(my, ry), px), half)), -1, c.D - 1);
-      vis = (fabs(amp) > tau) && ulo <= uhi && vlo <= vhi;
+      const double fu0 = fma(mx - rx, ipx, half), fu1 = fma(mx + rx, ipx, half);
+      const double fv0 = fma(my - ry, ipx, half), fv1 = fma(my + ry, ipx, half);
+      double cu0 = ceil(fu0), cu1 = floor(fu1), cv0 = ceil(fv0), cv1 = floor(fv1);
+      const double eps = 1e-9;
+      if (fabs(fu0 - rint(fu0)) < eps || fabs(fu1 - rint(fu1)) < eps || fabs(fv0 - rint(fv0)) < eps ||
+          fabs(fv1 - rint(fv1)) < eps) {  // canonical O3 evaluation (rare)
+        cu0 = ceil(da(dv(dsb(mx, rx), px), half));
+        cu1 = floor(da(dv(da(mx, rx), px), half));
+        cv0 = ceil(da(dv(dsb(my, ry), px), half));
+        cv1 = floor(da(dv(da(my, ry), px), half));
+      }
+      ulo = clip_d(cu0, 0, c.D);
+      uhi = clip_d(cu1, -1, c.D - 1);
+      vlo = clip_d(cv0, 0, c.D);
+      vhi = clip_d(cv1, -1, c.D - 1);
+      bool above = fabs(amp) > tau;
+      if (tau > 0.0 && fabs(fabs(amp) - tau) <= 1e-12 * tau) {  // canonical amplitude near the threshold
+        const double ampc = dm(rho, dm(kSqrt2Pi, sqrt(dv(g.detS, det2))));
+        above = fabs(ampc) > tau;
+      }
+      vis = above && ulo <= uhi && vlo <= vhi;
     }
     if (vis) {
       const double px2 = px * px;
-      double mxp = mx / px + half, myp = my / px + half;
+      double mxp = fma(mx, ipx, half), myp = fma(my, ipx, half);
       o.f0 = make_float4((float)(mxp - (double)ulo), (float)(myp - (double)vlo), (float)(Cc / det2 * px2),
                          (float)(-Bc / det2 * px2));
       o.f1 = make_float4((float)(A / det2 * px2), (float)amp, __int_as_float((ulo & 0xffff) | (uhi << 16)),
@@ -238,34 +260,66 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int *__restrict__ out
 }
 
 // --------------------------------------------------------------- a3 fill
-// One warp per (particle, chunk of 1024 Gaussians).  Gaussians are visited in
-// ascending j, 32 per step; each step's (j, tile) pairs are enumerated in
-// (j, tile) order and ranked per tile with __match_any_sync, so every list is
-// written in ascending j (a stable counting sort keyed by tile).
-__global__ void __launch_bounds__(32) k_fill(CfgDev c, const uint2 *__restrict__ box, const int *__restrict__ base,
-                                             int *__restrict__ ids) {
-  extern __shared__ int cnt[];
-  const int i = blockIdx.y, ch = blockIdx.x, lane = threadIdx.x;
-  for (int t = lane; t < c.NT; t += 32) cnt[t] = base[((size_t)i * c.NT + t) * c.C + ch];
-  __syncwarp();
+// One CTA of 4 warps per (particle, chunk of 1024 Gaussians); warp w owns the
+// 256-Gaussian sub-chunk w.  Pass 1 counts each sub-chunk's entries per tile
+// (smem integer atomics, order-free); a per-tile scan over the 4 sub-chunks,
+// seeded with the chunk's global offset, gives each warp its cursors; pass 2
+// visits the warp's Gaussians in ascending j, 32 per step, enumerates each
+// step's (j, tile) pairs in (j, tile) order and ranks them per tile with
+// __match_any_sync — a stable counting sort, so every list is ascending in j.
+constexpr int kFillWarps = 4, kSub = kChunk / kFillWarps;
+
+__device__ __forceinline__ void rect_of(uint2 b, int T, int &tu0, int &tu1, int &tv0, int &n) {
+  const int ulo = (int)(b.x & 0xffff), uhi = (int)(b.x >> 16), vlo = (int)(b.y & 0xffff), vhi = (int)(b.y >> 16);
+  if (ulo <= uhi && vlo <= vhi) {
+    tu0 = ulo / T; tu1 = uhi / T; tv0 = vlo / T;
+    n = (tu1 - tu0 + 1) * (vhi / T - tv0 + 1);
+  } else {
+    tu0 = 0; tu1 = -1; tv0 = 0; n = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 *__restrict__ box,
+                                                          const int *__restrict__ base, int *__restrict__ ids) {
+  extern __shared__ int cnt[];   // [kFillWarps][NT]
+  const int i = blockIdx.y, ch = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int *mine = cnt + w * c.NT;
+  for (int t = threadIdx.x; t < kFillWarps * c.NT; t += blockDim.x) cnt[t] = 0;
+  __syncthreads();
+  const int jsub = ch * kChunk + w * kSub;
+  const uint2 *boxi = box + (size_t)i * c.N;
+  for (int j = jsub + lane; j < min(jsub + kSub, c.N); j += 32) {   // pass 1: per-tile counts
+    int tu0, tu1, tv0, n;
+    rect_of(boxi[j], c.T, tu0, tu1, tv0, n);
+    const int wd = tu1 - tu0 + 1;
+    for (int r = 0; r < n; ++r) {
+      const int q = r / wd;
+      atomicAdd(&mine[(tv0 + q) * c.nt + tu0 + (r - q * wd)], 1);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < c.NT; t += blockDim.x) {
+    int run = base[((size_t)i * c.NT + t) * c.C + ch];
+#pragma unroll
+    for (int ww = 0; ww < kFillWarps; ++ww) {
+      const int v = cnt[ww * c.NT + t];
+      cnt[ww * c.NT + t] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
-  for (int step = 0; step < kChunk / 32; ++step) {
-    const int j0 = ch * kChunk + step * 32;
+  const float M = 12582912.f;
+  for (int step = 0; step < kSub / 32; ++step) {     // pass 2: stable fill
+    const int j0 = jsub + step * 32;
     if (j0 >= c.N) break;
     const int j = j0 + lane;
     int tu0 = 0, tu1 = -1, tv0 = 0, n = 0;
-    if (j < c.N) {
-      uint2 b = box[(size_t)i * c.N + j];
-      int ulo = (int)(b.x & 0xffff), uhi = (int)(b.x >> 16), vlo = (int)(b.y & 0xffff), vhi = (int)(b.y >> 16);
-      if (ulo <= uhi && vlo <= vhi) {
-        tu0 = ulo / c.T; tu1 = uhi / c.T; tv0 = vlo / c.T;
-        n = (tu1 - tu0 + 1) * (vhi / c.T - tv0 + 1);
-      }
-    }
+    if (j < c.N) rect_of(boxi[j], c.T, tu0, tu1, tv0, n);
     int incl = n;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, incl, d);
+      const int y = __shfl_up_sync(0xffffffffu, incl, d);
       if (lane >= d) incl += y;
     }
     const int excl = incl - n;
@@ -275,9 +329,9 @@ __global__ void __launch_bounds__(32) k_fill(CfgDev c, const uint2 *__restrict__
       const bool active = p < total;
       int lo = 0;
 #pragma unroll
-      for (int s = 16; s >= 1; s >>= 1) {
-        int vv = __shfl_sync(0xffffffffu, incl, lo + s - 1);
-        if (vv <= p) lo += s;
+      for (int sft = 16; sft >= 1; sft >>= 1) {
+        const int vv = __shfl_sync(0xffffffffu, incl, lo + sft - 1);
+        if (vv <= p) lo += sft;
       }
       const int owner = lo & 31;
       const int oex = __shfl_sync(0xffffffffu, excl, owner);
@@ -286,19 +340,20 @@ __global__ void __launch_bounds__(32) k_fill(CfgDev c, const uint2 *__restrict__
       const int otv0 = __shfl_sync(0xffffffffu, tv0, owner);
       int key = 0x40000000 + lane, t = 0;
       if (active) {
-        const int r = p - oex, w = otu1 - otu0 + 1;
-        t = (otv0 + r / w) * c.nt + (otu0 + r % w);
+        const int r = p - oex, wd = otu1 - otu0 + 1;
+        // q = r div wd exactly: round((r + 1/2)/wd - 1/2) with a magic-constant rounding
+        const int q = __float_as_int(fmaf((float)r + 0.5f, 1.0f / (float)wd, -0.5f) + M) - 0x4B400000;
+        t = (otv0 + q) * c.nt + otu0 + (r - q * wd);
         key = t;
       }
       const unsigned m = __match_any_sync(0xffffffffu, key);
       const int rank = __popc(m & lt);
-      int slot = 0;
       if (active) {
-        slot = cnt[t] + rank;
+        const int slot = mine[t] + rank;
         if ((int64_t)slot < c.cap) ids[slot] = j0 + owner;
       }
       __syncwarp();
-      if (active && rank == 0) cnt[t] += __popc(m);
+      if (active && rank == 0) mine[t] += __popc(m);
       __syncwarp();
     }
   }
@@ -330,7 +385,9 @@ void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, Dev
 
 void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, int *ids, cudaStream_t s, int &launches) {
   dim3 grid(c.C, B);
-  k_fill<<<grid, 32, c.NT * sizeof(int), s>>>(c, box, base, ids);
+  const size_t smem = (size_t)kFillWarps * c.NT * sizeof(int);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_fill<<<grid, kFillWarps * 32, smem, s>>>(c, box, base, ids);
   ++launches;
 }
 

@@ -43,6 +43,10 @@ __device__ __forceinline__ void red_add_v4(float4 *addr, float4 v) {
 // (bitwise deterministic).  Lane utilisation = |box ∩ tile| / 32 per pass.
 constexpr int kFwdWarps = 4;
 
+// Entries are processed in pairs with packed fp32 (FFMA2 / FADD2 / FMUL2):
+// the staging layout stores each field of a pair as one float2 so a pass needs
+// no register shuffling.
+
 template <int T>
 __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const SplatRec *__restrict__ rec,
                                                                 const int *__restrict__ base,
@@ -50,9 +54,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const S
                                                                 float *__restrict__ proj) {
   constexpr int S = T + 8;                     // accumulator row stride (floats)
   __shared__ float acc[kFwdWarps][T * S];
-  __shared__ float4 st0[kFwdWarps][32];        // (mx' + 1/2, my', A, B); mx' relative to the box∩tile corner
-  __shared__ float4 st1[kFwdWarps][32];        // (C, amp, 1/w, w)
-  __shared__ int2 st2[kFwdWarps][32];          // (npix, corner index | (S - w) << 16)
+  __shared__ float2 sf[kFwdWarps][8][17];      // [field][pair] = (entry a, entry b): mx', my', A, B, C, amp, 1/w, -w
+  __shared__ int4 si[kFwdWarps][17];           // (npix_a, npix_b, corner_a | sw_a << 16, corner_b | sw_b << 16)
   const int t = blockIdx.x, i = blockIdx.y, tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5;
   const int u0 = (t % c.nt) * T, v0 = (t / c.nt) * T;
@@ -73,46 +76,95 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const S
   const float laneh = (float)lane + 0.5f;
   const float M = 12582912.f;                   // 1.5 * 2^23: x + M rounds x to an integer
   float *accw = acc[w] + lane;
+  float2(*F)[17] = sf[w];
   __syncwarp();
-  for (int b0 = s + 32 * w; b0 < e; b0 += 32 * kFwdWarps) {
+  // software pipeline: the next batch's record is loaded while this batch renders
+  int b0 = s + 32 * w;
+  SplatRec nr;
+  int nid = -1;
+  if (b0 + lane < e) {
+    nid = ids[b0 + lane];
+    nr = reci[nid];
+  }
+  for (; b0 < e; b0 += 32 * kFwdWarps) {
     const int n = min(32, e - b0);
-    if (lane < n) {
-      const int id = ids[b0 + lane];
-      const SplatRec r = reci[id];
+    const SplatRec r = nr;
+    const bool have = lane < n;
+    const int nb = b0 + 32 * kFwdWarps + lane;
+    if (nb < e) {
+      nid = ids[nb];
+      nr = reci[nid];
+    }
+    int npix = 0, packed = 0;
+    float f[8];
+    if (have) {
       const int ub = __float_as_int(r.f1.z), vb = __float_as_int(r.f1.w);
       const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
-      const int bu0 = max(ulo - u0, 0), bu1 = min(uhi - u0, T - 1);
-      const int bv0 = max(vlo - v0, 0), bv1 = min(vhi - v0, T - 1);
-      const int wd = bu1 - bu0 + 1, ht = bv1 - bv0 + 1;
-      st0[w][lane] = make_float4((float)(ulo - u0 - bu0) + r.f0.x + 0.5f, (float)(vlo - v0 - bv0) + r.f0.y,
-                                 kA * r.f0.z, kB * r.f0.w);
-      st1[w][lane] = make_float4(kA * r.f1.x, r.f1.y, 1.0f / (float)wd, (float)wd);
-      st2[w][lane] = make_int2(wd * ht, (bv0 * S + bu0) | ((S - wd) << 16));
+      const int bu0 = max(ulo - u0, 0), bv0 = max(vlo - v0, 0);
+      const int wd = min(uhi - u0, T - 1) - bu0 + 1;
+      npix = wd * (min(vhi - v0, T - 1) - bv0 + 1);
+      packed = (bv0 * S + bu0) | ((S - wd) << 16);
+      f[0] = (float)(ulo - u0 - bu0) + r.f0.x + 0.5f;   // mx' + 1/2 (pixel index + 1/2 is enumerated)
+      f[1] = (float)(vlo - v0 - bv0) + r.f0.y;   // my'
+      f[2] = kA * r.f0.z;
+      f[3] = kB * r.f0.w;
+      f[4] = kA * r.f1.x;
+      f[5] = r.f1.y;
+      f[6] = 1.0f / (float)wd;
+      f[7] = -(float)wd;
+    }
+    // stage single-pass entries (npix <= 32) first so paired entries need equal passes
+    const unsigned big = __ballot_sync(0xffffffffu, have && npix > 32);
+    const unsigned small = __ballot_sync(0xffffffffu, have && npix <= 32);
+    const unsigned lt = (1u << lane) - 1u;
+    if (have) {
+      const int slot = npix > 32 ? __popc(small) + __popc(big & lt) : __popc(small & lt);
+      const int pr = slot >> 1, ab = slot & 1;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) reinterpret_cast<float *>(&F[q][pr])[ab] = f[q];
+      int *sip = (int *)&si[w][pr];
+      sip[ab] = npix;
+      sip[2 + ab] = packed;
+    }
+    if (lane == 0 && (n & 1)) {   // dummy partner for an odd count
+      int *sip = (int *)&si[w][n >> 1];
+      sip[1] = 0;
+      sip[3] = 0;
     }
     __syncwarp();
-    for (int k = 0; k < n; ++k) {
-      const float4 E0 = st0[w][k];
-      const float4 E1 = st1[w][k];
-      const int2 E2 = st2[w][k];
-      const int npix = E2.x, corner = E2.y & 0xffff, sw = E2.y >> 16;
-      float pfh = laneh;   // pixel index + 1/2
-      int p0 = 0;
+    const int npairs = (n + 1) >> 1;
+    for (int pr = 0; pr < npairs; ++pr) {
+      const int4 I = si[w][pr];
+      const float2 mx = F[0][pr], my = F[1][pr], A2 = F[2][pr], B2 = F[3][pr];
+      const float2 C2 = F[4][pr], amp = F[5][pr], iw = F[6][pr], nw = F[7][pr];
+      const int npm = max(I.x, I.y);
+      float2 pfh = make_float2(laneh, laneh);
+      float2 dxo = __fadd2_rn(pfh, make_float2(-mx.x, -mx.y));
+      float *pa = accw + (I.z & 0xffff), *pb = accw + (I.w & 0xffff);
+      const int swa = I.z >> 16, swb = I.w >> 16;
+      int p = lane;
 #pragma unroll 1
       do {
-        const float xm = fmaf(pfh, E1.z, -0.5f) + M;          // round((p + 1/2)/w - 1/2) = p div w
-        const float qf = xm - M;
-        const int qi = __float_as_int(xm) - 0x4B400000;
-        const float dx = fmaf(-qf, E1.w, pfh) - E0.x;            // (p mod w) - mx'
-        const float dy = qf - E0.y;
-        const float q = fmaf(fmaf(E0.z, dx, E0.w * dy), dx, E1.x * dy * dy);
-        const float ev = ex2(q);
-        if (p0 + lane < npix) {
-          float *a = accw + corner + p0 + qi * sw;
-          *a = fmaf(E1.y, ev, *a);
+        const float2 xm = __fadd2_rn(__ffma2_rn(pfh, iw, make_float2(-0.5f, -0.5f)), make_float2(M, M));
+        const float2 qf = __fadd2_rn(xm, make_float2(-M, -M));
+        const float2 dx = __ffma2_rn(qf, nw, dxo);
+        const float2 dy = __fadd2_rn(qf, make_float2(-my.x, -my.y));
+        const float2 q = __ffma2_rn(__ffma2_rn(A2, dx, __fmul2_rn(B2, dy)), dx, __fmul2_rn(__fmul2_rn(C2, dy), dy));
+        const float ea = ex2(q.x), eb = ex2(q.y);
+        if (p < I.x) {
+          float *a = pa + (__float_as_int(xm.x) - 0x4B400000) * swa;
+          *a = fmaf(amp.x, ea, *a);
         }
-        p0 += 32;
-        pfh += 32.f;
-      } while (p0 < npix);
+        if (p < I.y) {
+          float *b = pb + (__float_as_int(xm.y) - 0x4B400000) * swb;
+          *b = fmaf(amp.y, eb, *b);
+        }
+        p += 32;
+        pa += 32;
+        pb += 32;
+        pfh = __fadd2_rn(pfh, make_float2(32.f, 32.f));
+        dxo = __fadd2_rn(dxo, make_float2(32.f, 32.f));
+      } while (p - lane < npm);
     }
     __syncwarp();
   }
@@ -139,7 +191,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_render_bwd(CfgDev c, const Spla
                                                              const float *__restrict__ dldi,
                                                              const float4 *__restrict__ mean_rho,
                                                              const float *__restrict__ rot, float4 *__restrict__ acc) {
-  __shared__ float gs[T][T + 1];
+  __shared__ float gs[T + 1][T + 1];   // one spare row: the paired loop may read one past a row
   __shared__ float4 sr0[kBwdThreads], sr1[kBwdThreads];
   __shared__ int sid[kBwdThreads];
   __shared__ int hist[kBwdKeys];
@@ -218,26 +270,33 @@ __global__ void __launch_bounds__(kBwdThreads) k_render_bwd(CfgDev c, const Spla
       const float dx0 = (float)(ua - ulo) - mxr;
       float dy = (float)(va - vlo) - myr;
       const float *grow = &gs[va - v0][ua - u0];
-      const int nu = ubnd - ua;
+      const int nu = ubnd - ua;                 // row length - 1
+      const float2 na2 = make_float2(na, na), two = make_float2(2.f, 2.f);
 #pragma unroll 1
       for (int v = va; v <= vbnd; ++v, dy += 1.f, grow += T + 1) {
         const float t1 = nb2 * dy, t2 = nc * dy * dy;
-        float dx = dx0, T0 = 0.f, T1 = 0.f, T2 = 0.f;
+        const float2 t12 = make_float2(t1, t1), t22 = make_float2(t2, t2);
+        float2 dx = make_float2(dx0, dx0 + 1.f);
+        float2 T0 = make_float2(0.f, 0.f), T1 = T0, T2 = T0;
         const float *gp = grow;
 #pragma unroll 1
-        for (int uu = 0; uu <= nu; ++uu, dx += 1.f, ++gp) {
-          const float ge = *gp * ex2(fmaf(fmaf(na, dx, t1), dx, t2));
-          const float gdx = ge * dx;
-          T0 += ge;
-          T1 += gdx;
-          T2 = fmaf(gdx, dx, T2);
+        for (int uu = 0; uu <= nu; uu += 2, gp += 2) {   // two pixels per iteration (FFMA2)
+          const float2 arg = __ffma2_rn(__ffma2_rn(na2, dx, t12), dx, t22);
+          const float2 g2 = make_float2(gp[0], uu < nu ? gp[1] : 0.f);
+          const float2 ge = __fmul2_rn(g2, make_float2(ex2(arg.x), ex2(arg.y)));
+          const float2 gdx = __fmul2_rn(ge, dx);
+          T0 = __fadd2_rn(T0, ge);
+          T1 = __fadd2_rn(T1, gdx);
+          T2 = __ffma2_rn(gdx, dx, T2);
+          dx = __fadd2_rn(dx, two);
         }
-        A0 += T0;
-        A1 += T1;
-        A2 += T2;
-        Ay0 = fmaf(dy, T0, Ay0);
-        Ay1 = fmaf(dy, T1, Ay1);
-        Ayy0 = fmaf(dy * dy, T0, Ayy0);
+        const float s0 = T0.x + T0.y, s1 = T1.x + T1.y, s2 = T2.x + T2.y;
+        A0 += s0;
+        A1 += s1;
+        A2 += s2;
+        Ay0 = fmaf(dy, s0, Ay0);
+        Ay1 = fmaf(dy, s1, Ay1);
+        Ayy0 = fmaf(dy * dy, s0, Ayy0);
       }
       const float La = A0;
       const float Lmx = amp * fmaf(a, A1, b * Ay0), Lmy = amp * fmaf(b, A1, cc * Ay0);
