@@ -35,6 +35,7 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   if (c.eps == 0.f) c.eps = 1e-8f;
   d.D = c.D;
   d.T = c.tile;
+  d.tshift = c.tile == 16 ? 4 : 3;
   d.nt = (c.D + c.tile - 1) / c.tile;
   d.NT = d.nt * d.nt;
   d.N = (int)c.n_gauss;

@@ -51,7 +51,7 @@ struct DevStats {      // device-side counters (zeroed per forward)
 };
 
 struct CfgDev {        // resolved config passed by value to kernels
-  int D, T, nt, NT, N, C;
+  int D, T, tshift, nt, NT, N, C;   // T = 1 << tshift
   float px, k, tau;
   int64_t cap;
 };

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) k_splat_count(CfgDev c, const GaussPrep *
       o.f1 = make_float4((float)(A / det2 * px2), (float)amp, __int_as_float((ulo & 0xffff) | (uhi << 16)),
                          __int_as_float((vlo & 0xffff) | (vhi << 16)));
       pairs += (unsigned long long)(uhi - ulo + 1) * (unsigned long long)(vhi - vlo + 1);
-      const int tu0 = ulo / c.T, tu1 = uhi / c.T, tv0 = vlo / c.T, tv1 = vhi / c.T;
+      const int tu0 = (ulo >> c.tshift), tu1 = (uhi >> c.tshift), tv0 = (vlo >> c.tshift), tv1 = (vhi >> c.tshift);
       for (int tv = tv0; tv <= tv1; ++tv)
         for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&shist[tv * c.nt + tu], 1);
     } else {
@@ -269,11 +269,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int *__restrict__ out
 // __match_any_sync — a stable counting sort, so every list is ascending in j.
 constexpr int kFillWarps = 4, kSub = kChunk / kFillWarps;
 
-__device__ __forceinline__ void rect_of(uint2 b, int T, int &tu0, int &tu1, int &tv0, int &n) {
+__device__ __forceinline__ void rect_of(uint2 b, int ts, int &tu0, int &tu1, int &tv0, int &n) {
   const int ulo = (int)(b.x & 0xffff), uhi = (int)(b.x >> 16), vlo = (int)(b.y & 0xffff), vhi = (int)(b.y >> 16);
   if (ulo <= uhi && vlo <= vhi) {
-    tu0 = ulo / T; tu1 = uhi / T; tv0 = vlo / T;
-    n = (tu1 - tu0 + 1) * (vhi / T - tv0 + 1);
+    tu0 = ulo >> ts; tu1 = uhi >> ts; tv0 = vlo >> ts;
+    n = (tu1 - tu0 + 1) * ((vhi >> ts) - tv0 + 1);
   } else {
     tu0 = 0; tu1 = -1; tv0 = 0; n = 0;
   }
@@ -289,13 +289,12 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
   const int jsub = ch * kChunk + w * kSub;
   const uint2 *boxi = box + (size_t)i * c.N;
   for (int j = jsub + lane; j < min(jsub + kSub, c.N); j += 32) {   // pass 1: per-tile counts
-    int tu0, tu1, tv0, n;
-    rect_of(boxi[j], c.T, tu0, tu1, tv0, n);
-    const int wd = tu1 - tu0 + 1;
-    for (int r = 0; r < n; ++r) {
-      const int q = r / wd;
-      atomicAdd(&mine[(tv0 + q) * c.nt + tu0 + (r - q * wd)], 1);
-    }
+    const uint2 b = boxi[j];
+    const int ulo = (int)(b.x & 0xffff), uhi = (int)(b.x >> 16), vlo = (int)(b.y & 0xffff), vhi = (int)(b.y >> 16);
+    if (ulo > uhi || vlo > vhi) continue;
+    const int tu0 = (ulo >> c.tshift), tu1 = (uhi >> c.tshift), tv1 = (vhi >> c.tshift);
+    for (int tv = (vlo >> c.tshift); tv <= tv1; ++tv)
+      for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&mine[tv * c.nt + tu], 1);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < c.NT; t += blockDim.x) {
@@ -315,7 +314,8 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
     if (j0 >= c.N) break;
     const int j = j0 + lane;
     int tu0 = 0, tu1 = -1, tv0 = 0, n = 0;
-    if (j < c.N) rect_of(boxi[j], c.T, tu0, tu1, tv0, n);
+    if (j < c.N) rect_of(boxi[j], c.tshift, tu0, tu1, tv0, n);
+    const float rw = 1.0f / (float)max(tu1 - tu0 + 1, 1);   // once per lane and step
     int incl = n;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -338,11 +338,12 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
       const int otu0 = __shfl_sync(0xffffffffu, tu0, owner);
       const int otu1 = __shfl_sync(0xffffffffu, tu1, owner);
       const int otv0 = __shfl_sync(0xffffffffu, tv0, owner);
+      const float orw = __shfl_sync(0xffffffffu, rw, owner);
       int key = 0x40000000 + lane, t = 0;
       if (active) {
         const int r = p - oex, wd = otu1 - otu0 + 1;
         // q = r div wd exactly: round((r + 1/2)/wd - 1/2) with a magic-constant rounding
-        const int q = __float_as_int(fmaf((float)r + 0.5f, 1.0f / (float)wd, -0.5f) + M) - 0x4B400000;
+        const int q = __float_as_int(fmaf((float)r + 0.5f, orw, -0.5f) + M) - 0x4B400000;
         t = (otv0 + q) * c.nt + otu0 + (r - q * wd);
         key = t;
       }

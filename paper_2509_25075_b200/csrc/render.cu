@@ -26,6 +26,18 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
+}
+
 __device__ __forceinline__ void red_add_v4(float4 *addr, float4 v) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
@@ -54,8 +66,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const S
                                                                 float *__restrict__ proj) {
   constexpr int S = T + 8;                     // accumulator row stride (floats)
   __shared__ float acc[kFwdWarps][T * S];
-  __shared__ float2 sf[kFwdWarps][8][17];      // [field][pair] = (entry a, entry b): mx', my', A, B, C, amp, 1/w, -w
-  __shared__ int4 si[kFwdWarps][17];           // (npix_a, npix_b, corner_a | sw_a << 16, corner_b | sw_b << 16)
+  __shared__ float2 sf[kFwdWarps][8][17];      // [field][pair] = (entry a, entry b): mx'+1/2, my', A, B, C, amp, 1/w, -w
+  __shared__ int4 si[kFwdWarps][17];           // (npix_a, npix_b, byte offset a, byte offset b)
+  __shared__ int2 ssw[kFwdWarps][17];          // (4 (S - w_a), 4 (S - w_b)): byte stride correction per row
   const int t = blockIdx.x, i = blockIdx.y, tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5;
   const int u0 = (t % c.nt) * T, v0 = (t / c.nt) * T;
@@ -73,29 +86,21 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const S
   for (int k = lane; k < T * S; k += 32) acc[w][k] = 0.f;
   const SplatRec *reci = rec + (size_t)i * c.N;
   const float kA = -0.5f * kLog2e, kB = -kLog2e;
-  const float laneh = (float)lane + 0.5f;
   const float M = 12582912.f;                   // 1.5 * 2^23: x + M rounds x to an integer
-  float *accw = acc[w] + lane;
+  const uint32_t accb = smem_u32(&acc[w][lane]);
   float2(*F)[17] = sf[w];
   __syncwarp();
   // software pipeline: the next batch's record is loaded while this batch renders
   int b0 = s + 32 * w;
   SplatRec nr;
-  int nid = -1;
-  if (b0 + lane < e) {
-    nid = ids[b0 + lane];
-    nr = reci[nid];
-  }
+  if (b0 + lane < e) nr = reci[ids[b0 + lane]];
   for (; b0 < e; b0 += 32 * kFwdWarps) {
     const int n = min(32, e - b0);
     const SplatRec r = nr;
     const bool have = lane < n;
     const int nb = b0 + 32 * kFwdWarps + lane;
-    if (nb < e) {
-      nid = ids[nb];
-      nr = reci[nid];
-    }
-    int npix = 0, packed = 0;
+    if (nb < e) nr = reci[ids[nb]];
+    int npix = 0, boff = 0, bsw = 0;
     float f[8];
     if (have) {
       const int ub = __float_as_int(r.f1.z), vb = __float_as_int(r.f1.w);
@@ -103,9 +108,12 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const S
       const int bu0 = max(ulo - u0, 0), bv0 = max(vlo - v0, 0);
       const int wd = min(uhi - u0, T - 1) - bu0 + 1;
       npix = wd * (min(vhi - v0, T - 1) - bv0 + 1);
-      packed = (bv0 * S + bu0) | ((S - wd) << 16);
+      bsw = 4 * (S - wd);
+      // byte offset of the box corner, pre-biased so that offset + bits(xm) * bsw
+      // addresses row q = bits(xm) - bits(M) (wrap-around arithmetic)
+      boff = 4 * (bv0 * S + bu0) - 0x4B400000 * bsw;
       f[0] = (float)(ulo - u0 - bu0) + r.f0.x + 0.5f;   // mx' + 1/2 (pixel index + 1/2 is enumerated)
-      f[1] = (float)(vlo - v0 - bv0) + r.f0.y;   // my'
+      f[1] = (float)(vlo - v0 - bv0) + r.f0.y;          // my'
       f[2] = kA * r.f0.z;
       f[3] = kB * r.f0.w;
       f[4] = kA * r.f1.x;
@@ -124,24 +132,27 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const S
       for (int q = 0; q < 8; ++q) reinterpret_cast<float *>(&F[q][pr])[ab] = f[q];
       int *sip = (int *)&si[w][pr];
       sip[ab] = npix;
-      sip[2 + ab] = packed;
+      sip[2 + ab] = boff;
+      reinterpret_cast<int *>(&ssw[w][pr])[ab] = bsw;
     }
     if (lane == 0 && (n & 1)) {   // dummy partner for an odd count
       int *sip = (int *)&si[w][n >> 1];
       sip[1] = 0;
       sip[3] = 0;
+      reinterpret_cast<int *>(&ssw[w][n >> 1])[1] = 0;
     }
     __syncwarp();
     const int npairs = (n + 1) >> 1;
-    for (int pr = 0; pr < npairs; ++pr) {
+    const float laneh = (float)lane + 0.5f;
+    for (int pr = 0; pr < npairs; ++pr) {   // two entries per pass, packed fp32 (FFMA2)
       const int4 I = si[w][pr];
+      const int2 SW = ssw[w][pr];
       const float2 mx = F[0][pr], my = F[1][pr], A2 = F[2][pr], B2 = F[3][pr];
       const float2 C2 = F[4][pr], amp = F[5][pr], iw = F[6][pr], nw = F[7][pr];
       const int npm = max(I.x, I.y);
       float2 pfh = make_float2(laneh, laneh);
       float2 dxo = __fadd2_rn(pfh, make_float2(-mx.x, -mx.y));
-      float *pa = accw + (I.z & 0xffff), *pb = accw + (I.w & 0xffff);
-      const int swa = I.z >> 16, swb = I.w >> 16;
+      uint32_t pa = accb + (uint32_t)I.z, pb = accb + (uint32_t)I.w;
       int p = lane;
 #pragma unroll 1
       do {
@@ -152,16 +163,16 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const S
         const float2 q = __ffma2_rn(__ffma2_rn(A2, dx, __fmul2_rn(B2, dy)), dx, __fmul2_rn(__fmul2_rn(C2, dy), dy));
         const float ea = ex2(q.x), eb = ex2(q.y);
         if (p < I.x) {
-          float *a = pa + (__float_as_int(xm.x) - 0x4B400000) * swa;
-          *a = fmaf(amp.x, ea, *a);
+          const uint32_t a = pa + (uint32_t)__float_as_int(xm.x) * (uint32_t)SW.x;
+          sts_f32(a, fmaf(amp.x, ea, lds_f32(a)));
         }
         if (p < I.y) {
-          float *b = pb + (__float_as_int(xm.y) - 0x4B400000) * swb;
-          *b = fmaf(amp.y, eb, *b);
+          const uint32_t b = pb + (uint32_t)__float_as_int(xm.y) * (uint32_t)SW.y;
+          sts_f32(b, fmaf(amp.y, eb, lds_f32(b)));
         }
         p += 32;
-        pa += 32;
-        pb += 32;
+        pa += 128;
+        pb += 128;
         pfh = __fadd2_rn(pfh, make_float2(32.f, 32.f));
         dxo = __fadd2_rn(dxo, make_float2(32.f, 32.f));
       } while (p - lane < npm);
