@@ -379,7 +379,8 @@ gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_
   CK(cudaMemsetAsync(acc, 0, sizeof(float4) * 3 * (size_t)c.N, s));
   {
     Prof p(ctx, s, P_RENDER_BWD);
-    launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<int>(ctx, L.base), at<int>(ctx, L.ids),
+    launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<uint2>(ctx, L.box), at<int>(ctx, L.base),
+                      at<int>(ctx, L.ids),
                       at<float>(ctx, L.dldi), (const float4 *)params->mean_rho, at<float>(ctx, L.stage_rot), acc, s,
                       ctx->launches);
   }

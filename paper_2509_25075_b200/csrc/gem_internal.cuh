@@ -101,7 +101,7 @@ void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *b
 void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, float2 *spec_hat, const float2 *spec_obs,
                      float2 *spec_pred, double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
                      int &launches);
-void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids,
+void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const uint2 *box, const int *base, const int *ids,
                        const float *dldi, const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s,
                        int &launches);
 void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho, const float4 *log_scale,

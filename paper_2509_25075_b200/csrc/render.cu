@@ -191,23 +191,24 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const S
 }
 
 // Backward: one thread per list entry.  A warp's time is set by its largest
-// box ∩ tile, so each 256-entry chunk is first counting-sorted in smem by its
-// (height, width) class: threads of a warp then loop over near-equal boxes.
+// box ∩ tile, so the tile's whole list (up to kBwdMax entries per round) is first
+// counting-sorted in smem by the class (min(h,8), min(ceil(w/2),4)) of its box:
+// consecutive entries — one warp's — then have near-equal loop trip counts.
 constexpr int kBwdThreads = 256;
-constexpr int kBwdKeys = 144;   // (min(h,12)-1)*12 + min(w,12)-1
+constexpr int kBwdKeys = 32;
+constexpr int kBwdMax = 4096;
 
 template <int T>
 __global__ void __launch_bounds__(kBwdThreads) k_render_bwd(CfgDev c, const SplatRec *__restrict__ rec,
+                                                             const uint2 *__restrict__ box,
                                                              const int *__restrict__ base, const int *__restrict__ ids,
                                                              const float *__restrict__ dldi,
                                                              const float4 *__restrict__ mean_rho,
                                                              const float *__restrict__ rot, float4 *__restrict__ acc) {
   __shared__ float gs[T + 1][T + 1];   // one spare row: the paired loop may read one past a row
-  __shared__ float4 sr0[kBwdThreads], sr1[kBwdThreads];
-  __shared__ int sid[kBwdThreads];
+  __shared__ unsigned char skey[kBwdMax];
+  __shared__ unsigned short order[kBwdMax];
   __shared__ int hist[kBwdKeys];
-  __shared__ int order[kBwdThreads];
-  __shared__ int warp_tot[kBwdThreads / 32 + 1];
   const int t = blockIdx.x, i = blockIdx.y, tid = threadIdx.x;
   const int u0 = (t % c.nt) * T, v0 = (t / c.nt) * T;
   const size_t hidx = ((size_t)i * c.NT + t) * c.C;
@@ -229,119 +230,110 @@ __global__ void __launch_bounds__(kBwdThreads) k_render_bwd(CfgDev c, const Spla
   const float inv_px = 1.f / c.px, inv_px2 = inv_px * inv_px;
   const float nh = -0.5f * kLog2e;
   const SplatRec *reci = rec + (size_t)i * c.N;
-  const int lane = tid & 31, wid = tid >> 5;
-  for (int cs = s; cs < e; cs += kBwdThreads) {
-    const int n = min(kBwdThreads, e - cs);
-    for (int k = tid; k < kBwdKeys; k += kBwdThreads) hist[k] = 0;
+  const uint2 *boxi = box + (size_t)i * c.N;
+  for (int cs = s; cs < e; cs += kBwdMax) {
+    const int n = min(kBwdMax, e - cs);
+    if (tid < kBwdKeys) hist[tid] = 0;
     __syncthreads();
-    int key = 0;
-    if (tid < n) {
-      const int id = ids[cs + tid];
-      const SplatRec r = reci[id];
-      sid[tid] = id;
-      sr0[tid] = r.f0;
-      sr1[tid] = r.f1;
-      const int ub = __float_as_int(r.f1.z), vb = __float_as_int(r.f1.w);
-      const int wd = min(ub >> 16, u0 + T - 1) - max(ub & 0xffff, u0) + 1;
-      const int ht = min(vb >> 16, v0 + T - 1) - max(vb & 0xffff, v0) + 1;
-      key = (min(ht, 12) - 1) * 12 + (min(wd, 12) - 1);
+    for (int k = tid; k < n; k += kBwdThreads) {
+      const uint2 b = boxi[ids[cs + k]];
+      const int wd = min((int)(b.x >> 16), u0 + T - 1) - max((int)(b.x & 0xffff), u0) + 1;
+      const int ht = min((int)(b.y >> 16), v0 + T - 1) - max((int)(b.y & 0xffff), v0) + 1;
+      const int key = (min(ht, 8) - 1) * 4 + min((wd + 1) >> 1, 4) - 1;
+      skey[k] = (unsigned char)key;
       atomicAdd(&hist[key], 1);
     }
     __syncthreads();
-    // exclusive scan of the key histogram (one value per thread, kBwdKeys <= 256)
-    int hv = tid < kBwdKeys ? hist[tid] : 0, incl = hv;
+    if (tid < 32) {   // exclusive scan of the 32 class counts
+      const int hv = hist[tid];
+      int incl = hv;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += y;
-    }
-    if (lane == 31) warp_tot[wid] = incl;
-    __syncthreads();
-    int woff = 0;
-    for (int ww = 0; ww < wid; ++ww) woff += warp_tot[ww];
-    __syncthreads();
-    if (tid < kBwdKeys) hist[tid] = woff + incl - hv;
-    __syncthreads();
-    if (tid < n) order[atomicAdd(&hist[key], 1)] = tid;
-    __syncthreads();
-    if (tid < n) {
-      const int slot = order[tid];
-      const int id = sid[slot];
-      const float4 f0 = sr0[slot], f1 = sr1[slot];
-      const int ub = __float_as_int(f1.z), vb = __float_as_int(f1.w);
-      const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
-      const float mxr = f0.x, myr = f0.y, a = f0.z, b = f0.w, cc = f1.x, amp = f1.y;
-      const int ua = max(ulo, u0), ubnd = min(uhi, u0 + T - 1), va = max(vlo, v0), vbnd = min(vhi, v0 + T - 1);
-      // Per row (dy fixed) accumulate T0 = sum g e, T1 = sum g e dx, T2 = sum g e dx^2; since
-      // h = amp g e, the six partials are L_amp = sum T0 and, over rows,
-      // L_mx = amp (a sum T1 + b sum dy T0), L_my = amp (b sum T1 + c sum dy T0),
-      // L_a = -amp/2 sum T2, L_b = -amp sum dy T1, L_c = -amp/2 sum dy^2 T0.
-      const float na = nh * a, nb2 = 2.f * nh * b, nc = nh * cc;
-      float A0 = 0.f, A1 = 0.f, A2 = 0.f, Ay0 = 0.f, Ay1 = 0.f, Ayy0 = 0.f;
-      const float dx0 = (float)(ua - ulo) - mxr;
-      float dy = (float)(va - vlo) - myr;
-      const float *grow = &gs[va - v0][ua - u0];
-      const int nu = ubnd - ua;                 // row length - 1
-      const float2 na2 = make_float2(na, na), two = make_float2(2.f, 2.f);
-#pragma unroll 1
-      for (int v = va; v <= vbnd; ++v, dy += 1.f, grow += T + 1) {
-        const float t1 = nb2 * dy, t2 = nc * dy * dy;
-        const float2 t12 = make_float2(t1, t1), t22 = make_float2(t2, t2);
-        float2 dx = make_float2(dx0, dx0 + 1.f);
-        float2 T0 = make_float2(0.f, 0.f), T1 = T0, T2 = T0;
-        const float *gp = grow;
-#pragma unroll 1
-        for (int uu = 0; uu <= nu; uu += 2, gp += 2) {   // two pixels per iteration (FFMA2)
-          const float2 arg = __ffma2_rn(__ffma2_rn(na2, dx, t12), dx, t22);
-          const float2 g2 = make_float2(gp[0], uu < nu ? gp[1] : 0.f);
-          const float2 ge = __fmul2_rn(g2, make_float2(ex2(arg.x), ex2(arg.y)));
-          const float2 gdx = __fmul2_rn(ge, dx);
-          T0 = __fadd2_rn(T0, ge);
-          T1 = __fadd2_rn(T1, gdx);
-          T2 = __ffma2_rn(gdx, dx, T2);
-          dx = __fadd2_rn(dx, two);
-        }
-        const float s0 = T0.x + T0.y, s1 = T1.x + T1.y, s2 = T2.x + T2.y;
-        A0 += s0;
-        A1 += s1;
-        A2 += s2;
-        Ay0 = fmaf(dy, s0, Ay0);
-        Ay1 = fmaf(dy, s1, Ay1);
-        Ayy0 = fmaf(dy * dy, s0, Ayy0);
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (tid >= d) incl += y;
       }
-      const float La = A0;
-      const float Lmx = amp * fmaf(a, A1, b * Ay0), Lmy = amp * fmaf(b, A1, cc * Ay0);
-      float Lpa = amp * A2, Lpb = amp * Ay1, Lpc = amp * Ayy0;
-      Lpa *= -0.5f; Lpb = -Lpb; Lpc *= -0.5f;
-      // G_Sigma_hat (pixel units) = -K Gk K - 1/2 L_amp amp K, Gk = [[Lpa, Lpb/2],[Lpb/2, Lpc]]
-      const float g01 = 0.5f * Lpb;
-      const float KG00 = a * Lpa + b * g01, KG01 = a * g01 + b * Lpc;
-      const float KG10 = b * Lpa + cc * g01, KG11 = b * g01 + cc * Lpc;
-      const float hl = 0.5f * La * amp;
-      float G00 = -(KG00 * a + KG01 * b) - hl * a;
-      float G01 = -(KG00 * b + KG01 * cc) - hl * b;
-      float G11 = -(KG10 * b + KG11 * cc) - hl * cc;
-      G00 *= inv_px2; G01 *= inv_px2; G11 *= inv_px2;   // -> Angstrom units
-      const float lmx = Lmx * inv_px, lmy = Lmy * inv_px;
-      const float rho = mean_rho[id].w;
-      float4 o0, o1, o2;
-      o0.x = La * (amp / rho);
-      o0.y = lmx * W0[0] + lmy * W1[0];
-      o0.z = lmx * W0[1] + lmy * W1[1];
-      o0.w = lmx * W0[2] + lmy * W1[2];
-      // G_Sigma_kl = sum_ab W[a][k] G[a][b] W[b][l]
-      float M[3][3];
-  #pragma unroll
-      for (int kk = 0; kk < 3; ++kk)
-  #pragma unroll
-        for (int ll = kk; ll < 3; ++ll)
-          M[kk][ll] = W0[kk] * (G00 * W0[ll] + G01 * W1[ll]) + W1[kk] * (G01 * W0[ll] + G11 * W1[ll]);
-      o1 = make_float4(M[0][0], M[0][1], M[0][2], M[1][1]);
-      o2 = make_float4(M[1][2], M[2][2], 0.f, 0.f);
-      float4 *dst = acc + 3 * (size_t)id;
-      red_add_v4(dst, o0);
-      red_add_v4(dst + 1, o1);
-      red_add_v4(dst + 2, o2);
+      hist[tid] = incl - hv;
+    }
+    __syncthreads();
+    for (int k = tid; k < n; k += kBwdThreads) order[atomicAdd(&hist[skey[k]], 1)] = (unsigned short)k;
+    __syncthreads();
+    for (int kk = tid; kk < n; kk += kBwdThreads) {
+      const int id = ids[cs + order[kk]];
+      const SplatRec r = reci[id];
+      const int ub = __float_as_int(r.f1.z), vb = __float_as_int(r.f1.w);
+      const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
+      const float mxr = r.f0.x, myr = r.f0.y, a = r.f0.z, b = r.f0.w, cc = r.f1.x, amp = r.f1.y;
+    const int ua = max(ulo, u0), ubnd = min(uhi, u0 + T - 1), va = max(vlo, v0), vbnd = min(vhi, v0 + T - 1);
+    // Per row (dy fixed) accumulate T0 = sum g e, T1 = sum g e dx, T2 = sum g e dx^2; since
+    // h = amp g e, the six partials are L_amp = sum T0 and, over rows,
+    // L_mx = amp (a sum T1 + b sum dy T0), L_my = amp (b sum T1 + c sum dy T0),
+    // L_a = -amp/2 sum T2, L_b = -amp sum dy T1, L_c = -amp/2 sum dy^2 T0.
+    const float na = nh * a, nb2 = 2.f * nh * b, nc = nh * cc;
+    float A0 = 0.f, A1 = 0.f, A2 = 0.f, Ay0 = 0.f, Ay1 = 0.f, Ayy0 = 0.f;
+    const float dx0 = (float)(ua - ulo) - mxr;
+    float dy = (float)(va - vlo) - myr;
+    const float *grow = &gs[va - v0][ua - u0];
+    const int nu = ubnd - ua;                 // row length - 1
+    const float2 na2 = make_float2(na, na), two = make_float2(2.f, 2.f);
+#pragma unroll 1
+    for (int v = va; v <= vbnd; ++v, dy += 1.f, grow += T + 1) {
+      const float t1 = nb2 * dy, t2 = nc * dy * dy;
+      const float2 t12 = make_float2(t1, t1), t22 = make_float2(t2, t2);
+      float2 dx = make_float2(dx0, dx0 + 1.f);
+      float2 T0 = make_float2(0.f, 0.f), T1 = T0, T2 = T0;
+      const float *gp = grow;
+#pragma unroll 1
+      for (int uu = 0; uu <= nu; uu += 2, gp += 2) {   // two pixels per iteration (FFMA2)
+        const float2 arg = __ffma2_rn(__ffma2_rn(na2, dx, t12), dx, t22);
+        const float2 g2 = make_float2(gp[0], uu < nu ? gp[1] : 0.f);
+        const float2 ge = __fmul2_rn(g2, make_float2(ex2(arg.x), ex2(arg.y)));
+        const float2 gdx = __fmul2_rn(ge, dx);
+        T0 = __fadd2_rn(T0, ge);
+        T1 = __fadd2_rn(T1, gdx);
+        T2 = __ffma2_rn(gdx, dx, T2);
+        dx = __fadd2_rn(dx, two);
+      }
+      const float s0 = T0.x + T0.y, s1 = T1.x + T1.y, s2 = T2.x + T2.y;
+      A0 += s0;
+      A1 += s1;
+      A2 += s2;
+      Ay0 = fmaf(dy, s0, Ay0);
+      Ay1 = fmaf(dy, s1, Ay1);
+      Ayy0 = fmaf(dy * dy, s0, Ayy0);
+    }
+    const float La = A0;
+    const float Lmx = amp * fmaf(a, A1, b * Ay0), Lmy = amp * fmaf(b, A1, cc * Ay0);
+    float Lpa = amp * A2, Lpb = amp * Ay1, Lpc = amp * Ayy0;
+    Lpa *= -0.5f; Lpb = -Lpb; Lpc *= -0.5f;
+    // G_Sigma_hat (pixel units) = -K Gk K - 1/2 L_amp amp K, Gk = [[Lpa, Lpb/2],[Lpb/2, Lpc]]
+    const float g01 = 0.5f * Lpb;
+    const float KG00 = a * Lpa + b * g01, KG01 = a * g01 + b * Lpc;
+    const float KG10 = b * Lpa + cc * g01, KG11 = b * g01 + cc * Lpc;
+    const float hl = 0.5f * La * amp;
+    float G00 = -(KG00 * a + KG01 * b) - hl * a;
+    float G01 = -(KG00 * b + KG01 * cc) - hl * b;
+    float G11 = -(KG10 * b + KG11 * cc) - hl * cc;
+    G00 *= inv_px2; G01 *= inv_px2; G11 *= inv_px2;   // -> Angstrom units
+    const float lmx = Lmx * inv_px, lmy = Lmy * inv_px;
+    const float rho = mean_rho[id].w;
+    float4 o0, o1, o2;
+    o0.x = La * (amp / rho);
+    o0.y = lmx * W0[0] + lmy * W1[0];
+    o0.z = lmx * W0[1] + lmy * W1[1];
+    o0.w = lmx * W0[2] + lmy * W1[2];
+    // G_Sigma_kl = sum_ab W[a][k] G[a][b] W[b][l]
+    float M[3][3];
+#pragma unroll
+    for (int kk = 0; kk < 3; ++kk)
+#pragma unroll
+      for (int ll = kk; ll < 3; ++ll)
+        M[kk][ll] = W0[kk] * (G00 * W0[ll] + G01 * W1[ll]) + W1[kk] * (G01 * W0[ll] + G11 * W1[ll]);
+    o1 = make_float4(M[0][0], M[0][1], M[0][2], M[1][1]);
+    o2 = make_float4(M[1][2], M[2][2], 0.f, 0.f);
+    float4 *dst = acc + 3 * (size_t)id;
+    red_add_v4(dst, o0);
+    red_add_v4(dst + 1, o1);
+    red_add_v4(dst + 2, o2);
     }
     __syncthreads();
   }
@@ -357,12 +349,12 @@ void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *b
   ++launches;
 }
 
-void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids,
+void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const uint2 *box, const int *base, const int *ids,
                        const float *dldi, const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s,
                        int &launches) {
   dim3 grid(c.NT, B);
-  if (c.T == 16) k_render_bwd<16><<<grid, kBwdThreads, 0, s>>>(c, rec, base, ids, dldi, mean_rho, rot, acc);
-  else k_render_bwd<8><<<grid, kBwdThreads, 0, s>>>(c, rec, base, ids, dldi, mean_rho, rot, acc);
+  if (c.T == 16) k_render_bwd<16><<<grid, kBwdThreads, 0, s>>>(c, rec, box, base, ids, dldi, mean_rho, rot, acc);
+  else k_render_bwd<8><<<grid, kBwdThreads, 0, s>>>(c, rec, box, base, ids, dldi, mean_rho, rot, acc);
   ++launches;
 }
 
