@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--tile", type=int, default=16)
     ap.add_argument("--state", default="steady", choices=["steady", "init"])
     ap.add_argument("--ring", type=int, default=1024, help="distinct device-resident particles per GPU")
+    ap.add_argument("--fused", action="store_true", help="L2-resident wave pipeline (GEM_FLAG_FUSED)")
+    ap.add_argument("--wave", type=int, default=0, help="particles per wave (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -210,7 +212,7 @@ def main():
     params = gem.SoA.from_arrays(mr, ls, q, dev)
     phantom = gem.SoA.from_arrays(*synth.f32(*synth.phantom(w, synth.seed_for(w.name, "phantom", 0))), dev)
     cfg = gem.GemConfig(D=w.D, pixel_size=px, n_gauss=w.N, max_batch=B, tile=args.tile,
-                        lr_mean=1e-3 * w.ball_radius)
+                        lr_mean=1e-3 * w.ball_radius, fused=args.fused, wave=args.wave)
 
     # device-resident ring of distinct synthetic particles (per-rank seeds)
     rot_np, sh_np, ctf_np = synth.f32(*synth.particles(w, ring, 1000 + rank))
@@ -311,12 +313,13 @@ def main():
     roof = None
     if dominant in ("render_fwd", "render_bwd"):
         per_pair = FLOP_FWD_PAIR if dominant == "render_fwd" else FLOP_BWD_PAIR
-        avg_s = kern[dominant][1] / kern[dominant][0] / 1e3
-        achieved = per_pair * pairs / avg_s / 1e12
+        avg_s = kern[dominant][1] / kern[dominant][0] / 1e3          # per launch (one wave)
+        achieved = per_pair * pairs * args.steps / (kern[dominant][1] / 1e3) / 1e12
         peak = fp32_peak_tflops(sm_max)
         roof = {"bound": "alu", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
-                "work_per_launch": f"{per_pair} FP32 FLOP x {pairs} useful (Gaussian, pixel) pairs",
+                "work_per_launch": f"{per_pair} FP32 FLOP x {pairs} useful (Gaussian, pixel) pairs per step, "
+                                   f"{kern[dominant][0] // max(args.steps, 1)} launch(es) per step",
                 "avg_launch_ms": avg_s * 1e3,
                 "peak_source": f"148 SMs x 128 FP32 lanes x 2 FLOP/FMA x {sm_max:.0f} MHz ({peak_src} sm_max_mhz)"}
     elif dominant is not None:
@@ -336,6 +339,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{w.name}: EMPIAR-10028-shaped, N={w.N} Gaussians, D={w.D}, px={w.px} A",
                    "model_state": args.state, "batch_per_gpu": B, "global_batch": B * world, "tile": args.tile,
+                   "fused_waves": args.fused, "wave": int(st["wave"]),
                    "ring_particles_per_gpu": ring, "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2: per-step working set (splat records "
                          f"{B * w.N * 32 / 1e6:.0f} MB + images) and a {ring}-particle ring "

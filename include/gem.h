@@ -82,8 +82,18 @@ typedef struct {
   int64_t list_capacity;  /* max (Gaussian, tile) entries per batch (0 -> derived)          */
   float lr_mean, lr_log_scale, lr_quat, lr_density; /* Adam learning rates per class       */
   float beta1, beta2, eps;                          /* Adam (0 -> 0.9, 0.999, 1e-8)         */
-  uint32_t flags;         /* reserved, 0                                                  */
+  uint32_t flags;         /* GEM_FLAG_* below                                              */
+  int32_t wave;           /* particles per L2-resident wave in fused mode (0 = auto)        */
 } gem_config;
+
+/* gem_config.flags.  GEM_FLAG_FUSED: gem_forward processes the batch in waves
+ * of `wave` particles, running splat -> cull/bin -> projection -> FFT/CTF/loss
+ * -> C2R -> backward scatter per wave so that splat records, tile lists and
+ * images stay resident in L2; gem_backward then only finalizes the gradient
+ * from the accumulators.  Results are those of the unfused path (same
+ * arithmetic; the scatter's atomic order differs).  In fused mode
+ * gem_export_lists can only export particles of the last wave. */
+enum { GEM_FLAG_FUSED = 1 };
 
 /* Gaussian parameter store (a0): three float4 arrays of length N.
  *   mean_rho [N] = (mu_x, mu_y, mu_z [Angstrom], rho)
@@ -121,6 +131,8 @@ typedef struct {
   int64_t workspace_bytes;
   int64_t pairs;          /* useful (Gaussian, pixel) pairs of the last forward: sum over
                              visible (i,j) of the AABB area (the algorithmic work unit)      */
+  int32_t wave;           /* particles per wave in use                                      */
+  int32_t fused;          /* 1 if GEM_FLAG_FUSED                                            */
 } gem_stats_t;
 
 /* Per-kernel device time recorded with CUDA events on the launching stream

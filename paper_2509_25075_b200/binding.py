@@ -15,6 +15,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "gem.h")
 GEM_OK, GEM_E_INVALID, GEM_E_SHAPE, GEM_E_ALIGN, GEM_E_CUDA, GEM_E_CUFFT, GEM_E_CAPACITY, GEM_E_STATE, \
     GEM_E_NONFINITE = range(9)
 GEM_MEM_DEVICE, GEM_MEM_HOST = 0, 1
+GEM_FLAG_FUSED = 1
 
 
 class GemConfigC(ctypes.Structure):
@@ -23,7 +24,7 @@ class GemConfigC(ctypes.Structure):
                 ("tile", ctypes.c_int32), ("list_capacity", ctypes.c_int64),
                 ("lr_mean", ctypes.c_float), ("lr_log_scale", ctypes.c_float), ("lr_quat", ctypes.c_float),
                 ("lr_density", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
-                ("eps", ctypes.c_float), ("flags", ctypes.c_uint32)]
+                ("eps", ctypes.c_float), ("flags", ctypes.c_uint32), ("wave", ctypes.c_int32)]
 
 
 class GemSoaC(ctypes.Structure):
@@ -38,7 +39,8 @@ class GemBatchC(ctypes.Structure):
 class GemStatsC(ctypes.Structure):
     _fields_ = [("entries", ctypes.c_int64), ("capacity", ctypes.c_int64), ("degenerate", ctypes.c_int32),
                 ("overflow", ctypes.c_int32), ("nonfinite", ctypes.c_int32), ("batch", ctypes.c_int32),
-                ("workspace_bytes", ctypes.c_int64), ("pairs", ctypes.c_int64)]
+                ("workspace_bytes", ctypes.c_int64), ("pairs", ctypes.c_int64), ("wave", ctypes.c_int32),
+                ("fused", ctypes.c_int32)]
 
 
 class GemKernelTimeC(ctypes.Structure):

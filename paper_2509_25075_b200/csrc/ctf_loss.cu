@@ -129,12 +129,16 @@ __global__ void __launch_bounds__(1024) k_loss_reduce(int B, int nblk, const dou
 }  // namespace
 
 void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, float2 *spec_hat, const float2 *spec_obs,
-                     float2 *spec_pred, double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
-                     int &launches) {
+                     float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches) {
   dim3 grid(loss_blocks, B);
   k_ctf_loss<<<grid, kCtfThreads, 0, s>>>(c, ctf, spec_hat, spec_obs, spec_pred, loss_part);
+  ++launches;
+}
+
+void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
+                        int &launches) {
   k_loss_reduce<<<1, 1024, 0, s>>>(B, loss_blocks, loss_part, loss, st);
-  launches += 2;
+  ++launches;
 }
 
 int ctf_loss_blocks(int D) { return (D * (D / 2 + 1) + kCtfThreads - 1) / kCtfThreads; }

@@ -8,13 +8,6 @@
 
 #include "gem_internal.cuh"
 
-namespace gem {
-void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, float2 *spec_hat, const float2 *spec_obs,
-                     float2 *spec_pred, double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
-                     int &launches);
-int ctf_loss_blocks(int D);
-}  // namespace gem
-
 using namespace gem;
 
 namespace {
@@ -43,8 +36,20 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   d.px = c.pixel_size;
   d.k = c.cull_k;
   d.tau = c.tau;
-  if (c.list_capacity <= 0)
-    c.list_capacity = (int64_t)c.max_batch * ((c.tile == 16 ? 6 : 12) * (int64_t)d.N + d.NT);
+  if (c.flags & ~(uint32_t)GEM_FLAG_FUSED) return false;
+  if (c.flags & GEM_FLAG_FUSED) {
+    if (c.wave <= 0) {   // auto: keep one wave's splat records, lists and images within ~64 MB of L2
+      const double per = (double)d.N * (32 + 8 + 4 * (c.tile == 16 ? 2 : 3)) + (double)c.D * c.D * 4 * 3 +
+                         (double)c.D * (c.D / 2 + 1) * 8 * 2;
+      c.wave = (int32_t)(64.0 * 1024 * 1024 / per);
+    }
+    if (c.wave < 1) c.wave = 1;
+    if (c.wave > c.max_batch) c.wave = c.max_batch;
+  } else {
+    c.wave = c.max_batch;
+  }
+  if (c.list_capacity <= 0)   // per wave (= per batch when not fused)
+    c.list_capacity = (int64_t)c.wave * ((c.tile == 16 ? 6 : 12) * (int64_t)d.N + d.NT);
   if (c.list_capacity > 0x7fffffffll) c.list_capacity = 0x7fffffffll;
   d.cap = c.list_capacity;
   return true;
@@ -63,9 +68,9 @@ bool make_plan(int D, int B, cufftType type, cufftHandle *h, size_t *ws) {
 
 Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   Layout L{};
-  const size_t Bm = (size_t)c.max_batch, N = (size_t)d.N, D = (size_t)d.D;
+  const size_t Bm = (size_t)c.max_batch, W = (size_t)c.wave, N = (size_t)d.N, D = (size_t)d.D;
   const size_t H = D * (D / 2 + 1);
-  L.n_hist = (int64_t)Bm * d.NT * d.C;
+  L.n_hist = (int64_t)W * d.NT * d.C;
   L.n_scan_blk = (L.n_hist + 4095) / 4096;
   L.list_cap = c.list_capacity;
   L.loss_blocks = ctf_loss_blocks(d.D);
@@ -73,17 +78,17 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
   L.prep = take(sizeof(GaussPrep) * N);
-  L.rec = take(sizeof(SplatRec) * Bm * N);
-  L.box = take(sizeof(uint2) * Bm * N);
+  L.rec = take(sizeof(SplatRec) * W * N);
+  L.box = take(sizeof(uint2) * W * N);
   L.hist = take(sizeof(int) * (size_t)L.n_hist);
   L.base = take(sizeof(int) * ((size_t)L.n_hist + 1));
   L.scan_blk = take(sizeof(int) * ((size_t)L.n_scan_blk + 1));
   L.ids = take(sizeof(int) * (size_t)L.list_cap);
-  L.proj = take(sizeof(float) * Bm * D * D);
-  L.spec_hat = take(sizeof(float2) * Bm * H);
-  L.spec_obs = take(sizeof(float2) * Bm * H);
-  L.spec_pred = take(sizeof(float2) * Bm * H);
-  L.dldi = take(sizeof(float) * Bm * D * D);
+  L.proj = take(sizeof(float) * W * D * D);
+  L.spec_hat = take(sizeof(float2) * W * H);
+  L.spec_obs = take(sizeof(float2) * W * H);
+  L.spec_pred = take(sizeof(float2) * W * H);
+  L.dldi = take(sizeof(float) * W * D * D);
   L.acc = take(sizeof(float4) * 3 * N);
   L.loss_part = take(sizeof(double) * Bm * (size_t)L.loss_blocks);
   L.stats = take(sizeof(DevStats));
@@ -210,7 +215,7 @@ size_t gem_workspace_bytes(const gem_config *cfg) {
   CfgDev d;
   if (!resolve(cfg, c, d)) return 0;
   size_t cb = 0;
-  if (!cufft_sizes(c.D, c.max_batch, &cb)) return 0;
+  if (!cufft_sizes(c.D, c.wave, &cb)) return 0;
   return layout(c, d, cb).total;
 }
 
@@ -223,7 +228,7 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
   if (!workspace) return GEM_E_INVALID;
   if (((uintptr_t)workspace & 255u) != 0) return GEM_E_ALIGN;
   size_t cb = 0;
-  if (!cufft_sizes(c.D, c.max_batch, &cb)) return GEM_E_CUFFT;
+  if (!cufft_sizes(c.D, c.wave, &cb)) return GEM_E_CUFFT;
   Layout L = layout(c, d, cb);
   if (bytes < L.total) return GEM_E_SHAPE;
   gem_ctx *ctx = new (std::nothrow) gem_ctx();
@@ -235,8 +240,10 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
   ctx->ws_bytes = bytes;
   ctx->stream = (cudaStream_t)stream;
   ctx->n_plans = 0;
+  ctx->W = c.wave;
+  ctx->fused = (c.flags & GEM_FLAG_FUSED) ? 1 : 0;
   cufftHandle a, b;
-  gem_status st = plan_for(ctx, c.max_batch, &a, &b);
+  gem_status st = plan_for(ctx, c.wave, &a, &b);
   if (st != GEM_OK) { delete ctx; return st; }
   if (cudaMemsetAsync(ctx->ws + L.stats, 0, sizeof(DevStats), ctx->stream) != cudaSuccess ||
       cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
@@ -326,39 +333,56 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
   }
   DevStats *st = at<DevStats>(ctx, L.stats);
   CK(cudaMemsetAsync(st, 0, sizeof(DevStats), s));
-  cufftHandle r2c, c2r;
-  gem_status ps = plan_for(ctx, B, &r2c, &c2r);
-  if (ps != GEM_OK) return ps;
   GaussPrep *prep = at<GaussPrep>(ctx, L.prep);
   SplatRec *rec = at<SplatRec>(ctx, L.rec);
   uint2 *box = at<uint2>(ctx, L.box);
   int *hist = at<int>(ctx, L.hist), *base = at<int>(ctx, L.base), *ids = at<int>(ctx, L.ids);
-  { Prof p(ctx, s, P_PREP); launch_prep(c, (const float4 *)params->log_scale, (const float4 *)params->quat, prep, st, s, ctx->launches); }
-  { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, B, prep, (const float4 *)params->mean_rho, rot, shift, rec, box, hist, st, s, ctx->launches); }
-  const int64_t nh = (int64_t)B * c.NT * c.C;
-  { Prof p(ctx, s, P_SCAN); launch_scan(hist, base, nh, at<int>(ctx, L.scan_blk), (nh + 4095) / 4096, st, c.cap, s, ctx->launches); }
-  { Prof p(ctx, s, P_FILL); launch_fill(c, B, box, base, ids, s, ctx->launches); }
-  float *proj = proj_out ? proj_out : at<float>(ctx, L.proj);
-  { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, B, rec, base, ids, proj, s, ctx->launches); }
   float2 *sh = at<float2>(ctx, L.spec_hat), *so = at<float2>(ctx, L.spec_obs), *sp = at<float2>(ctx, L.spec_pred);
-  CKF(cufftSetStream(r2c, s));
-  CKF(cufftSetStream(c2r, s));
-  {
-    Prof p(ctx, s, P_FFT_R2C);
-    CKF(cufftExecR2C(r2c, (cufftReal *)proj, (cufftComplex *)sh));
-    CKF(cufftExecR2C(r2c, (cufftReal *)obs, (cufftComplex *)so));
+  float *dldi = at<float>(ctx, L.dldi);
+  float4 *acc = at<float4>(ctx, L.acc);
+  double *lpart = at<double>(ctx, L.loss_part);
+  if (ctx->fused) CK(cudaMemsetAsync(acc, 0, sizeof(float4) * 3 * (size_t)c.N, s));
+  { Prof p(ctx, s, P_PREP); launch_prep(c, (const float4 *)params->log_scale, (const float4 *)params->quat, prep, st, s, ctx->launches); }
+  const size_t DD = D * D;
+  int p0 = 0, nb = 0;
+  for (p0 = 0; p0 < B; p0 += ctx->W) {   // one wave (all of B when not fused)
+    nb = B - p0 < ctx->W ? B - p0 : ctx->W;
+    cufftHandle r2c, c2r;
+    gem_status ps = plan_for(ctx, nb, &r2c, &c2r);
+    if (ps != GEM_OK) return ps;
+    const float *rw = rot + 9 * (size_t)p0;
+    { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist, st, s, ctx->launches); }
+    const int64_t nh = (int64_t)nb * c.NT * c.C;
+    { Prof p(ctx, s, P_SCAN); launch_scan(hist, base, nh, at<int>(ctx, L.scan_blk), (nh + 4095) / 4096, st, c.cap, s, ctx->launches); }
+    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, ids, s, ctx->launches); }
+    float *proj = proj_out ? proj_out + p0 * DD : at<float>(ctx, L.proj);
+    { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, base, ids, proj, s, ctx->launches); }
+    CKF(cufftSetStream(r2c, s));
+    CKF(cufftSetStream(c2r, s));
+    {
+      Prof p(ctx, s, P_FFT_R2C);
+      CKF(cufftExecR2C(r2c, (cufftReal *)proj, (cufftComplex *)sh));
+      CKF(cufftExecR2C(r2c, (cufftReal *)(obs + p0 * DD), (cufftComplex *)so));
+    }
+    {
+      Prof p(ctx, s, P_CTF_LOSS);
+      launch_ctf_loss(c, nb, ctf + 8 * (size_t)p0, sh, so, pred_out ? sp : nullptr, lpart + (size_t)p0 * L.loss_blocks,
+                      L.loss_blocks, s, ctx->launches);
+    }
+    {
+      Prof p(ctx, s, P_FFT_C2R);
+      if (pred_out) CKF(cufftExecC2R(c2r, (cufftComplex *)sp, (cufftReal *)(pred_out + p0 * DD)));
+      CKF(cufftExecC2R(c2r, (cufftComplex *)sh, (cufftReal *)dldi));
+    }
+    if (ctx->fused) {
+      Prof p(ctx, s, P_RENDER_BWD);
+      launch_render_bwd(c, nb, rec, box, base, ids, dldi, (const float4 *)params->mean_rho, rw, acc, s, ctx->launches);
+    }
   }
+  ctx->last_p0 = p0 - ctx->W;
+  ctx->last_nb = nb;
   double *lossd = host ? at<double>(ctx, L.stage_loss) : loss;
-  {
-    Prof p(ctx, s, P_CTF_LOSS);
-    launch_ctf_loss(c, B, ctf, sh, so, pred_out ? sp : nullptr, at<double>(ctx, L.loss_part), L.loss_blocks, lossd,
-                    st, s, ctx->launches);
-  }
-  {
-    Prof p(ctx, s, P_FFT_C2R);
-    if (pred_out) CKF(cufftExecC2R(c2r, (cufftComplex *)sp, (cufftReal *)pred_out));
-    CKF(cufftExecC2R(c2r, (cufftComplex *)sh, (cufftReal *)at<float>(ctx, L.dldi)));
-  }
+  { Prof p(ctx, s, P_CTF_LOSS); launch_loss_reduce(B, lpart, L.loss_blocks, lossd, st, s, ctx->launches); }
   if (host) CK(cudaMemcpyAsync(loss, lossd, sizeof(double) * (B + 1), cudaMemcpyDeviceToHost, s));
   CK(cudaGetLastError());
   ctx->fwd_live = 1;
@@ -376,8 +400,8 @@ gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_
   const CfgDev &c = ctx->dc;
   const Layout &L = ctx->L;
   float4 *acc = at<float4>(ctx, L.acc);
-  CK(cudaMemsetAsync(acc, 0, sizeof(float4) * 3 * (size_t)c.N, s));
-  {
+  if (!ctx->fused) {   // fused mode: the forward already scattered every wave into acc
+    CK(cudaMemsetAsync(acc, 0, sizeof(float4) * 3 * (size_t)c.N, s));
     Prof p(ctx, s, P_RENDER_BWD);
     launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<uint2>(ctx, L.box), at<int>(ctx, L.base),
                       at<int>(ctx, L.ids),
@@ -447,6 +471,8 @@ gem_status gem_export_lists(gem_ctx *ctx, int32_t particle, int32_t *tile_off, i
   if (!ctx) return GEM_E_INVALID;
   if (!ctx->fwd_live) return GEM_E_STATE;
   if (particle < 0 || particle >= ctx->last_B) return GEM_E_SHAPE;
+  if (particle < ctx->last_p0 || particle >= ctx->last_p0 + ctx->last_nb) return GEM_E_STATE;  // not resident
+  particle -= ctx->last_p0;
   CK(cudaStreamSynchronize(ctx->stream));
   const CfgDev &c = ctx->dc;
   const Layout &L = ctx->L;
@@ -502,6 +528,8 @@ gem_status gem_stats(gem_ctx *ctx, gem_stats_t *out) {
   out->batch = ctx->last_B;
   out->workspace_bytes = (int64_t)ctx->ws_bytes;
   out->pairs = (int64_t)h.pairs;
+  out->wave = ctx->W;
+  out->fused = ctx->fused;
   if (h.overflow) return GEM_E_CAPACITY;
   if (h.nonfinite) return GEM_E_NONFINITE;
   return GEM_OK;

@@ -73,6 +73,9 @@ struct gem_ctx {
   int n_plans;
   int fwd_live;        // a forward's lists/records/dL/dI are valid
   int last_B;
+  int W;               // particles per wave (max_batch when not fused)
+  int fused;           // GEM_FLAG_FUSED
+  int last_p0, last_nb;  // the last wave of the last forward
   int launches;
   // profiling (gem_profile_enable): event pairs around launches
   int prof_on;
@@ -99,8 +102,10 @@ void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, int 
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
                        cudaStream_t s, int &launches);
 void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, float2 *spec_hat, const float2 *spec_obs,
-                     float2 *spec_pred, double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
-                     int &launches);
+                     float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches);
+void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
+                        int &launches);
+int ctf_loss_blocks(int D);
 void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const uint2 *box, const int *base, const int *ids,
                        const float *dldi, const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s,
                        int &launches);

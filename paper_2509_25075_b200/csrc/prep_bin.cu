@@ -245,10 +245,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_blocks(int *__restrict__ 
     if (b < nblk) blk[b] = e + carry;
     carry += total;
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {   // totals accumulate over the waves of one forward
     out[n] = carry;
-    st->entries = (unsigned long long)carry;
-    st->overflow = (int64_t)carry > cap ? 1 : 0;
+    st->entries += (unsigned long long)carry;
+    if ((int64_t)carry > cap) st->overflow = 1;
   }
 }
 

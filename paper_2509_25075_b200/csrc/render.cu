@@ -44,33 +44,32 @@ __device__ __forceinline__ void red_add_v4(float4 *addr, float4 v) {
 }
 
 
-// Warp-per-entry forward.  Each warp takes batches of 32 consecutive list
-// entries (batch b -> warp b % kFwdWarps), stages them in its own smem slot,
-// and for each entry enumerates the pixels of AABB_j ∩ tile linearly over its
-// 32 lanes (pixel p = pass*32 + lane -> row q = p / w, col r = p % w, computed
-// exactly in fp32 with a round-to-nearest magic constant).  Values are added
-// into a warp-private tile accumulator in smem: within a warp the lanes of one
-// pass touch distinct pixels and entries are processed in order, so no atomics
-// are needed; the kFwdWarps copies are summed in a fixed order at the end
-// (bitwise deterministic).  Lane utilisation = |box ∩ tile| / 32 per pass.
+// Row-owner forward.  Each warp takes batches of 32 list entries strided over the
+// tile's list (batch j -> warp j % kFwdWarps) and stages them in smem.  Lane l owns tile
+// row q = l % T of accumulator copy l / T (32/T private copies per warp), and
+// walks the row segments AABB_k ∩ row q of the batch's entries of its copy
+// (entry k -> copy k % (32/T)) in ascending k: for one segment it evaluates
+// amp exp(-Q/2) along the row, two columns per iteration with packed fp32
+// (FFMA2).  All lanes of a round work on distinct (copy, row) accumulators, so
+// there are no write conflicts and no atomics; the per-warp copies are summed in
+// a fixed order at the end (bitwise deterministic).  Lane utilisation is the
+// fraction of rows with a segment in the round times mean/max segment width.
 constexpr int kFwdWarps = 4;
-
-// Entries are processed in pairs with packed fp32 (FFMA2 / FADD2 / FMUL2):
-// the staging layout stores each field of a pair as one float2 so a pass needs
-// no register shuffling.
 
 template <int T>
 __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const SplatRec *__restrict__ rec,
                                                                 const int *__restrict__ base,
                                                                 const int *__restrict__ ids,
                                                                 float *__restrict__ proj) {
-  constexpr int S = T + 8;                     // accumulator row stride (floats)
-  __shared__ float acc[kFwdWarps][T * S];
-  __shared__ float2 sf[kFwdWarps][8][17];      // [field][pair] = (entry a, entry b): mx'+1/2, my', A, B, C, amp, 1/w, -w
-  __shared__ int4 si[kFwdWarps][17];           // (npix_a, npix_b, byte offset a, byte offset b)
-  __shared__ int2 ssw[kFwdWarps][17];          // (4 (S - w_a), 4 (S - w_b)): byte stride correction per row
+  constexpr int S = T + 1;                    // accumulator row stride (floats)
+  constexpr int NCP = 32 / T;                 // accumulator copies per warp (one lane per row each)
+  constexpr int COPY = T * S;
+  __shared__ float acc[kFwdWarps][NCP * COPY];
+  __shared__ float4 st0[kFwdWarps][32];       // (bu0 - mx', my', na, nb2)  tile-local, pre-scaled conic
+  __shared__ float4 st1[kFwdWarps][32];       // (nc, amp, bu0 | w << 8, -)
   const int t = blockIdx.x, i = blockIdx.y, tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5;
+  const int q = lane % T, cp = lane / T;
   const int u0 = (t % c.nt) * T, v0 = (t / c.nt) * T;
   const size_t hidx = ((size_t)i * c.NT + t) * c.C;
   int s = base[hidx], e = base[hidx + c.C];
@@ -83,99 +82,71 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const S
     }
     return;
   }
-  for (int k = lane; k < T * S; k += 32) acc[w][k] = 0.f;
+  for (int k = lane; k < NCP * COPY; k += 32) acc[w][k] = 0.f;
   const SplatRec *reci = rec + (size_t)i * c.N;
-  const float kA = -0.5f * kLog2e, kB = -kLog2e;
-  const float M = 12582912.f;                   // 1.5 * 2^23: x + M rounds x to an integer
-  const uint32_t accb = smem_u32(&acc[w][lane]);
-  float2(*F)[17] = sf[w];
+  const float nh = -0.5f * kLog2e;
+  const uint32_t rowb = smem_u32(&acc[w][cp * COPY + q * S]);
+  const unsigned csel = (NCP == 2 ? 0x55555555u : (NCP == 4 ? 0x11111111u : 0x01010101u)) << cp;
+  const float qf = (float)q;
   __syncwarp();
-  // software pipeline: the next batch's record is loaded while this batch renders
-  int b0 = s + 32 * w;
+  // Batch j (j = 0 .. nbat-1, warp j % kFwdWarps) holds entries s + j + nbat * l, l = 0..31:
+  // strided over the whole (spatially ordered) list, so a batch's boxes spread over all
+  // rows of the tile and the per-row segment counts stay balanced across lanes.
+  const int nlist = e - s, nbat = (nlist + 31) >> 5;
+  int j = w;
   SplatRec nr;
-  if (b0 + lane < e) nr = reci[ids[b0 + lane]];
-  for (; b0 < e; b0 += 32 * kFwdWarps) {
-    const int n = min(32, e - b0);
+  if (j < nbat && j + nbat * lane < nlist) nr = reci[ids[s + j + nbat * lane]];
+  for (; j < nbat; j += kFwdWarps) {
+    const bool have = j + nbat * lane < nlist;
     const SplatRec r = nr;
-    const bool have = lane < n;
-    const int nb = b0 + 32 * kFwdWarps + lane;
-    if (nb < e) nr = reci[ids[nb]];
-    int npix = 0, boff = 0, bsw = 0;
-    float f[8];
+    const int jn = j + kFwdWarps;
+    if (jn < nbat && jn + nbat * lane < nlist) nr = reci[ids[s + jn + nbat * lane]];
+    int bv0 = T, bv1 = -1;
     if (have) {
       const int ub = __float_as_int(r.f1.z), vb = __float_as_int(r.f1.w);
       const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
-      const int bu0 = max(ulo - u0, 0), bv0 = max(vlo - v0, 0);
-      const int wd = min(uhi - u0, T - 1) - bu0 + 1;
-      npix = wd * (min(vhi - v0, T - 1) - bv0 + 1);
-      bsw = 4 * (S - wd);
-      // byte offset of the box corner, pre-biased so that offset + bits(xm) * bsw
-      // addresses row q = bits(xm) - bits(M) (wrap-around arithmetic)
-      boff = 4 * (bv0 * S + bu0) - 0x4B400000 * bsw;
-      f[0] = (float)(ulo - u0 - bu0) + r.f0.x + 0.5f;   // mx' + 1/2 (pixel index + 1/2 is enumerated)
-      f[1] = (float)(vlo - v0 - bv0) + r.f0.y;          // my'
-      f[2] = kA * r.f0.z;
-      f[3] = kB * r.f0.w;
-      f[4] = kA * r.f1.x;
-      f[5] = r.f1.y;
-      f[6] = 1.0f / (float)wd;
-      f[7] = -(float)wd;
+      const int bu0 = max(ulo - u0, 0), wd = min(uhi - u0, T - 1) - bu0 + 1;
+      bv0 = max(vlo - v0, 0);
+      bv1 = min(vhi - v0, T - 1);
+      const float mx = (float)(ulo - u0) + r.f0.x, my = (float)(vlo - v0) + r.f0.y;
+      st0[w][lane] = make_float4((float)bu0 - mx, my, nh * r.f0.z, 2.f * nh * r.f0.w);
+      st1[w][lane] = make_float4(nh * r.f1.x, r.f1.y, __int_as_float(bu0 | (wd << 8)), 0.f);
     }
-    // stage single-pass entries (npix <= 32) first so paired entries need equal passes
-    const unsigned big = __ballot_sync(0xffffffffu, have && npix > 32);
-    const unsigned small = __ballot_sync(0xffffffffu, have && npix <= 32);
-    const unsigned lt = (1u << lane) - 1u;
-    if (have) {
-      const int slot = npix > 32 ? __popc(small) + __popc(big & lt) : __popc(small & lt);
-      const int pr = slot >> 1, ab = slot & 1;
+    unsigned mine = 0;   // entries of this batch whose box covers my row, of my copy
 #pragma unroll
-      for (int q = 0; q < 8; ++q) reinterpret_cast<float *>(&F[q][pr])[ab] = f[q];
-      int *sip = (int *)&si[w][pr];
-      sip[ab] = npix;
-      sip[2 + ab] = boff;
-      reinterpret_cast<int *>(&ssw[w][pr])[ab] = bsw;
+    for (int rr = 0; rr < T; ++rr) {
+      const unsigned m = __ballot_sync(0xffffffffu, bv0 <= rr && rr <= bv1);
+      if (rr == q) mine = m;
     }
-    if (lane == 0 && (n & 1)) {   // dummy partner for an odd count
-      int *sip = (int *)&si[w][n >> 1];
-      sip[1] = 0;
-      sip[3] = 0;
-      reinterpret_cast<int *>(&ssw[w][n >> 1])[1] = 0;
-    }
+    mine &= csel;
     __syncwarp();
-    const int npairs = (n + 1) >> 1;
-    const float laneh = (float)lane + 0.5f;
-    for (int pr = 0; pr < npairs; ++pr) {   // two entries per pass, packed fp32 (FFMA2)
-      const int4 I = si[w][pr];
-      const int2 SW = ssw[w][pr];
-      const float2 mx = F[0][pr], my = F[1][pr], A2 = F[2][pr], B2 = F[3][pr];
-      const float2 C2 = F[4][pr], amp = F[5][pr], iw = F[6][pr], nw = F[7][pr];
-      const int npm = max(I.x, I.y);
-      float2 pfh = make_float2(laneh, laneh);
-      float2 dxo = __fadd2_rn(pfh, make_float2(-mx.x, -mx.y));
-      uint32_t pa = accb + (uint32_t)I.z, pb = accb + (uint32_t)I.w;
-      int p = lane;
 #pragma unroll 1
-      do {
-        const float2 xm = __fadd2_rn(__ffma2_rn(pfh, iw, make_float2(-0.5f, -0.5f)), make_float2(M, M));
-        const float2 qf = __fadd2_rn(xm, make_float2(-M, -M));
-        const float2 dx = __ffma2_rn(qf, nw, dxo);
-        const float2 dy = __fadd2_rn(qf, make_float2(-my.x, -my.y));
-        const float2 q = __ffma2_rn(__ffma2_rn(A2, dx, __fmul2_rn(B2, dy)), dx, __fmul2_rn(__fmul2_rn(C2, dy), dy));
-        const float ea = ex2(q.x), eb = ex2(q.y);
-        if (p < I.x) {
-          const uint32_t a = pa + (uint32_t)__float_as_int(xm.x) * (uint32_t)SW.x;
-          sts_f32(a, fmaf(amp.x, ea, lds_f32(a)));
-        }
-        if (p < I.y) {
-          const uint32_t b = pb + (uint32_t)__float_as_int(xm.y) * (uint32_t)SW.y;
-          sts_f32(b, fmaf(amp.y, eb, lds_f32(b)));
-        }
-        p += 32;
-        pa += 128;
-        pb += 128;
-        pfh = __fadd2_rn(pfh, make_float2(32.f, 32.f));
-        dxo = __fadd2_rn(dxo, make_float2(32.f, 32.f));
-      } while (p - lane < npm);
+    while (__any_sync(0xffffffffu, mine != 0)) {
+      int wd = 0;
+      float4 E0 = make_float4(0.f, 0.f, 0.f, 0.f), E1 = E0;
+      if (mine) {
+        const int k = __ffs(mine) - 1;
+        mine &= mine - 1;
+        E0 = st0[w][k];
+        E1 = st1[w][k];
+        wd = __float_as_int(E1.z) >> 8;
+      }
+      const int wmax = __reduce_max_sync(0xffffffffu, wd);
+      const float dy = qf - E0.y;
+      const float t1 = E0.w * dy, t2 = E1.x * dy * dy;
+      const float2 na2 = make_float2(E0.z, E0.z), t12 = make_float2(t1, t1), t22 = make_float2(t2, t2);
+      float2 dx = make_float2(E0.x, E0.x + 1.f);
+      const uint32_t a0 = rowb + 4u * (uint32_t)(__float_as_int(E1.z) & 0xff);
+      const float amp = E1.y;
+#pragma unroll 1
+      for (int cc = 0; cc < wmax; cc += 2) {
+        const float2 arg = __ffma2_rn(__ffma2_rn(na2, dx, t12), dx, t22);
+        const float ea = ex2(arg.x), eb = ex2(arg.y);
+        const uint32_t a = a0 + 4u * (uint32_t)cc;
+        if (cc < wd) sts_f32(a, fmaf(amp, ea, lds_f32(a)));
+        if (cc + 1 < wd) sts_f32(a + 4u, fmaf(amp, eb, lds_f32(a + 4u)));
+        dx = __fadd2_rn(dx, make_float2(2.f, 2.f));
+      }
     }
     __syncwarp();
   }
@@ -184,7 +155,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const S
     const int pu = pp % T, pv = pp / T;
     float sum = 0.f;
 #pragma unroll
-    for (int ww = 0; ww < kFwdWarps; ++ww) sum += acc[ww][pv * S + pu];
+    for (int ww = 0; ww < kFwdWarps; ++ww)
+#pragma unroll
+      for (int k = 0; k < NCP; ++k) sum += acc[ww][k * COPY + pv * S + pu];
     const int u = u0 + pu, v = v0 + pv;
     if (u < c.D && v < c.D) proj[((size_t)i * c.D + v) * c.D + u] = sum;
   }

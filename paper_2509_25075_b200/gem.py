@@ -32,11 +32,13 @@ class GemConfig:
     beta1: float = 0.9
     beta2: float = 0.999
     eps: float = 1e-8
+    fused: bool = False   # L2-resident wave pipeline (GEM_FLAG_FUSED)
+    wave: int = 0         # particles per wave (0 = auto)
 
     def c(self) -> _b.GemConfigC:
         return _b.GemConfigC(self.D, self.pixel_size, self.n_gauss, self.max_batch, self.cull_k, self.tau, self.tile,
                              self.list_capacity, self.lr_mean, self.lr_log_scale, self.lr_quat, self.lr_density,
-                             self.beta1, self.beta2, self.eps, 0)
+                             self.beta1, self.beta2, self.eps, _b.GEM_FLAG_FUSED if self.fused else 0, self.wave)
 
 
 class SoA:

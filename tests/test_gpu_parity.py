@@ -42,10 +42,11 @@ def make_case(wname="T", B=4, seed=0, N=None, D=None, state="steady", morton=Tru
     return dict(w=w, params=(mr, ls, q), rot=rot, shift=shift, ctf=ctf, obs=obs, px=float(np.float32(w.px)))
 
 
-def run_gpu(gem, case, tile=16, want_lists=False, cap=0, host=False):
+def run_gpu(gem, case, tile=16, want_lists=False, cap=0, host=False, fused=False, wave=0):
     w = case["w"]
     B = case["rot"].shape[0]
-    cfg = gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=B, tile=tile, list_capacity=cap)
+    cfg = gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=B, tile=tile, list_capacity=cap,
+                        fused=fused, wave=wave)
     st = gem.GemStep(cfg)
     dev = st.device
     P = gem.SoA.from_arrays(*case["params"], device=dev)
@@ -63,7 +64,9 @@ def run_gpu(gem, case, tile=16, want_lists=False, cap=0, host=False):
     out = dict(st=st, P=P, loss=loss.cpu().numpy().copy(), proj=proj.cpu().numpy(), pred=pred.cpu().numpy(),
                grad=grad.t.permute(1, 0, 2).reshape(w.N, 12).cpu().numpy(), grad_soa=grad)
     if want_lists:
-        out["lists"] = [st.export_lists(i) for i in range(B)]
+        first = 0 if not fused else B - ((B - 1) % wave + 1)   # only the last wave is resident when fused
+        out["lists"] = [st.export_lists(i) for i in range(first, B)]
+        out["lists_first"] = first
     out["stats"] = st.stats(check=False)
     return out
 
@@ -78,12 +81,13 @@ def maxnorm_rel(a, b):
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
 
 
-def assert_lists_exact(orc, case, lists, tile):
+def assert_lists_exact(orc, case, lists, tile, first=0):
     w = case["w"]
     aabb, vis, sp = orc.splats(case["params"], case["rot"], case["shift"], w.D, case["px"])
     tile_off, base, ids = orc.lists(aabb, vis, w.D, tile)
     ties = 0
-    for i, (g_off, g_ids, g_box) in enumerate(lists):
+    for ii, (g_off, g_ids, g_box) in enumerate(lists):
+        i = first + ii
         g_vis = (g_box[:, 0] <= g_box[:, 1]) & (g_box[:, 2] <= g_box[:, 3])
         bad = np.nonzero((g_vis != vis[i].astype(bool)) |
                          (vis[i].astype(bool) & np.any(g_box != aabb[i], axis=1)))[0]
@@ -102,12 +106,12 @@ def assert_lists_exact(orc, case, lists, tile):
 
 
 # --------------------------------------------------------------------------- tests
-@pytest.mark.parametrize("tile", [16, 8])
-def test_T_lists_images_loss_grads(gem, orc, tile):
+@pytest.mark.parametrize("tile,fused", [(16, False), (8, False), (16, True), (8, True)])
+def test_T_lists_images_loss_grads(gem, orc, tile, fused):
     case = make_case("T", B=6, seed=1)
-    g = run_gpu(gem, case, tile=tile, want_lists=True)
+    g = run_gpu(gem, case, tile=tile, want_lists=True, fused=fused, wave=4 if fused else 0)   # waves of 4 + 2
     assert g["stats"]["status"] == 0, g["stats"]
-    assert_lists_exact(orc, case, g["lists"], tile)
+    assert_lists_exact(orc, case, g["lists"], tile, g["lists_first"])
     o = oracle_out(orc, case)
     for i in range(case["rot"].shape[0]):
         assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
@@ -160,8 +164,8 @@ def test_init_state_and_unsorted_ids(gem, orc):
 
 def test_S_config_two_particles(gem, orc):
     case = make_case("S", B=2, seed=4)
-    g = run_gpu(gem, case, want_lists=True)
-    assert_lists_exact(orc, case, g["lists"], 16)
+    g = run_gpu(gem, case, want_lists=True, fused=True, wave=1)
+    assert_lists_exact(orc, case, g["lists"], 16, g["lists_first"])
     o = oracle_out(orc, case)
     for i in range(2):
         assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
