@@ -78,7 +78,7 @@ typedef struct {
   int32_t max_batch;      /* max particles per gem_forward, >= 1                          */
   float cull_k;           /* Mahalanobis radius of the AABB cull (0 -> 3)                  */
   float tau;              /* |amp| <= tau => culled (Eq. 8); >= 0            */
-  int32_t tile;           /* tile edge for the per-tile lists: 8 or 16 (0 -> 16)          */
+  int32_t tile;           /* tile edge for the per-tile lists: 8 or 16 (0 -> 8)           */
   int64_t list_capacity;  /* max (Gaussian, tile) entries per batch (0 -> derived)          */
   float lr_mean, lr_log_scale, lr_quat, lr_density; /* Adam learning rates per class       */
   float beta1, beta2, eps;                          /* Adam (0 -> 0.9, 0.999, 1e-8)         */

@@ -21,7 +21,7 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   if (c.max_batch < 1 || c.max_batch > 65535) return false;
   if (c.cull_k == 0.f) c.cull_k = 3.f;
   if (!(c.cull_k > 0.f) || !(c.tau >= 0.f)) return false;
-  if (c.tile == 0) c.tile = 16;
+  if (c.tile == 0) c.tile = 8;
   if (c.tile != 8 && c.tile != 16) return false;
   if (c.beta1 == 0.f) c.beta1 = 0.9f;
   if (c.beta2 == 0.f) c.beta2 = 0.999f;
@@ -89,9 +89,12 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.spec_obs = take(sizeof(float2) * W * H);
   L.spec_pred = take(sizeof(float2) * W * H);
   L.dldi = take(sizeof(float) * W * D * D);
+  L.slot_a = take(sizeof(float4) * W * N);   // backward image-space partials [i][j]
+  L.slot_b = take(sizeof(float2) * W * N);
   L.acc = take(sizeof(float4) * 3 * N);
   L.loss_part = take(sizeof(double) * Bm * (size_t)L.loss_blocks);
   L.stats = take(sizeof(DevStats));
+  L.ticket = take(64);   // persistent-kernel work tickets (self-resetting; zeroed at init)
   L.stage_rot = take(sizeof(float) * 9 * Bm);
   L.stage_shift = take(sizeof(float) * 2 * Bm);
   L.stage_ctf = take(sizeof(float) * 8 * Bm);
@@ -155,7 +158,7 @@ gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r) {
 
 // ---- profiling: an event pair around each launch group while enabled
 const char *kProfNames[P_COUNT] = {"prep", "splat_count", "scan", "fill", "render_fwd", "fft_r2c",
-                                   "ctf_loss", "fft_c2r", "render_bwd", "finalize", "adam", "volume"};
+                                   "ctf_loss", "fft_c2r", "render_bwd", "bwd_reduce", "finalize", "adam", "volume"};
 
 struct Prof {
   gem_ctx *ctx;
@@ -246,6 +249,7 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
   gem_status st = plan_for(ctx, c.wave, &a, &b);
   if (st != GEM_OK) { delete ctx; return st; }
   if (cudaMemsetAsync(ctx->ws + L.stats, 0, sizeof(DevStats), ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(ctx->ws + L.ticket, 0, 64, ctx->stream) != cudaSuccess ||
       cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
     gem_destroy(ctx);
     return GEM_E_CUDA;
@@ -356,7 +360,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     { Prof p(ctx, s, P_SCAN); launch_scan(hist, base, nh, at<int>(ctx, L.scan_blk), (nh + 4095) / 4096, st, c.cap, s, ctx->launches); }
     { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, ids, s, ctx->launches); }
     float *proj = proj_out ? proj_out + p0 * DD : at<float>(ctx, L.proj);
-    { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, base, ids, proj, s, ctx->launches); }
+    { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, base, ids, proj, at<int>(ctx, L.ticket), s, ctx->launches); }
     CKF(cufftSetStream(r2c, s));
     CKF(cufftSetStream(c2r, s));
     {
@@ -375,8 +379,13 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
       CKF(cufftExecC2R(c2r, (cufftComplex *)sh, (cufftReal *)dldi));
     }
     if (ctx->fused) {
-      Prof p(ctx, s, P_RENDER_BWD);
-      launch_render_bwd(c, nb, rec, box, base, ids, dldi, (const float4 *)params->mean_rho, rw, acc, s, ctx->launches);
+      {
+        Prof p(ctx, s, P_RENDER_BWD);
+        launch_render_bwd(c, nb, rec, dldi, at<float4>(ctx, L.slot_a), at<float2>(ctx, L.slot_b), s, ctx->launches);
+      }
+      Prof p(ctx, s, P_BWD_REDUCE);
+      launch_bwd_reduce(c, nb, at<float4>(ctx, L.slot_a), at<float2>(ctx, L.slot_b),
+                        (const float4 *)params->mean_rho, rw, acc, s, ctx->launches);
     }
   }
   ctx->last_p0 = p0 - ctx->W;
@@ -402,11 +411,14 @@ gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_
   float4 *acc = at<float4>(ctx, L.acc);
   if (!ctx->fused) {   // fused mode: the forward already scattered every wave into acc
     CK(cudaMemsetAsync(acc, 0, sizeof(float4) * 3 * (size_t)c.N, s));
-    Prof p(ctx, s, P_RENDER_BWD);
-    launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<uint2>(ctx, L.box), at<int>(ctx, L.base),
-                      at<int>(ctx, L.ids),
-                      at<float>(ctx, L.dldi), (const float4 *)params->mean_rho, at<float>(ctx, L.stage_rot), acc, s,
-                      ctx->launches);
+    {
+      Prof p(ctx, s, P_RENDER_BWD);
+      launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<float>(ctx, L.dldi), at<float4>(ctx, L.slot_a),
+                        at<float2>(ctx, L.slot_b), s, ctx->launches);
+    }
+    Prof p(ctx, s, P_BWD_REDUCE);
+    launch_bwd_reduce(c, ctx->last_B, at<float4>(ctx, L.slot_a), at<float2>(ctx, L.slot_b),
+                      (const float4 *)params->mean_rho, at<float>(ctx, L.stage_rot), acc, s, ctx->launches);
   }
   Prof pf(ctx, s, P_FINALIZE);
   launch_finalize(c, acc, (const float4 *)params->mean_rho, (const float4 *)params->log_scale,

@@ -32,8 +32,8 @@ struct __align__(16) SplatRec {
 };
 
 struct Layout {  // byte offsets into the caller's workspace
-  size_t prep, rec, box, hist, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, acc, loss_part,
-      stats, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, total;
+  size_t prep, rec, box, hist, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slot_a, slot_b, acc, loss_part,
+      stats, ticket, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, total;
   int64_t n_hist;       // B_max * NT * C
   int64_t n_scan_blk;
   int64_t list_cap;
@@ -86,7 +86,7 @@ struct gem_ctx {
 
 namespace gem {
 enum ProfKind { P_PREP, P_SPLAT, P_SCAN, P_FILL, P_RENDER_FWD, P_FFT_R2C, P_CTF_LOSS, P_FFT_C2R, P_RENDER_BWD,
-                P_FINALIZE, P_ADAM, P_VOLUME, P_COUNT };
+                P_BWD_REDUCE, P_FINALIZE, P_ADAM, P_VOLUME, P_COUNT };
 }
 
 // ---------------------------------------------------------------- kernels
@@ -100,15 +100,16 @@ void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, Dev
                  int &launches);
 void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, int *ids, cudaStream_t s, int &launches);
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
-                       cudaStream_t s, int &launches);
+                       int *ticket, cudaStream_t s, int &launches);
 void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, float2 *spec_hat, const float2 *spec_obs,
                      float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches);
 void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
                         int &launches);
 int ctf_loss_blocks(int D);
-void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const uint2 *box, const int *base, const int *ids,
-                       const float *dldi, const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s,
-                       int &launches);
+void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float *dldi, float4 *slotA, float2 *slotB,
+                       cudaStream_t s, int &launches);
+void launch_bwd_reduce(const CfgDev &c, int B, const float4 *slotA, const float2 *slotB,
+                       const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s, int &launches);
 void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho, const float4 *log_scale,
                      const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
                      int &launches);

@@ -1,20 +1,12 @@
-// render.cu — a5 forward evaluate/project and a7 backward scatter over the
-// per-tile lists.
+// render.cu — a5 forward evaluate/project, a7 backward over the per-tile lists, and the
+// per-Gaussian reduction of the backward's image-space partials.
 //
 // Forward (Eq. 6 with the Eq. 8 selection):
 //   I_hat(u,v) = sum_{j in list(tile(u,v)), (u,v) in AABB_j} amp_j exp(-Q_j/2),
 //   Q = a dx^2 + 2 b dx dy + c dy^2 (pixel units).
-// One CTA (4 warps) per (particle, T x T tile); see k_render_fwd below for the
-// warp-per-entry scheme (lanes over the pixels of one entry's box, warp-private
-// smem accumulators, fixed-order reduction: bitwise deterministic).
-//
-// Backward ("gradient computation restricted to the Gaussians contributing to
-// each pixel"): one thread per list entry loops over the
-// pixels of AABB_j inside the tile (dL/dI_hat staged in smem), accumulating four
-// per-row sums from which the six partials (L_amp, L_mx, L_my, L_a, L_b, L_c)
-// follow algebraically; it then transforms them to
-// world-frame accumulators (L_rho, G_mu, G_Sigma; DESIGN.md §3 O9) and adds
-// them with three vector reductions red.global.add.v4.f32.
+// Backward: per (particle, Gaussian), the moments of dL/dI_hat * exp(-Q/2)
+// over AABB_ij give the six 2D partials; see k_render_bwd and k_bwd_reduce.
+// Both use multiplicative recurrences instead of one exp per pixel (see the forward's comment).
 #include "gem_internal.cuh"
 
 namespace gem {
@@ -26,308 +18,419 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+// Forward.  Recurrences: in pixel units, with f = log2 of the kernel, f(dx, dy) = na dx^2 +
+// nb2 dx dy + nc dy^2 (na = -log2(e) a / 2, nb2 = -log2(e) b, nc = -log2(e) c / 2), f is quadratic
+// along a row and along a column, so the values on the pixel grid obey exact multiplicative
+// recurrences:
+//   along a row                  e_{k+1} = e_k R_k,  R_{k+1} = R_k S,  S  = 2^{2 na}
+//   down the box's first column  e_{r+1} = e_r V_r,  V_{r+1} = V_r W,  W  = 2^{2 nc}
+//   and the row ratio            R(r+1) = R(r) Kb,                     Kb = 2^{nb2}.
+// One (Gaussian x tile) entry costs 6 exps plus two multiplies per pixel instead of one exp per
+// pixel (MUFU: 16/clk/SM vs 128 FMA lanes/clk/SM; tools/microbench.cu).  Rounding: a pixel k
+// columns and r rows from the box corner carries ~(k^2 + r^2)/4 ulp relative to its own value.
+// Safety: f <= 0, so values never overflow; the recurrences stay exact only while their factors
+// are normal numbers, so an entry whose first-column values fall below 2^-100 amp (needle-like
+// Gaussians at far AABB corners), whose corner row ratio is below 2^-120, whose W, Kb leave the
+// normal range, or whose amplitude is negative is evaluated directly (exp per pixel).
+constexpr int kFwdWarps = 2;       // warps per CTA (independent)
+constexpr int kCH = 64;            // list entries staged per chunk per warp
+
+__device__ __forceinline__ int next_item(int *ticket, int lane) {
+  int item = 0;
+  if (lane == 0) item = atomicAdd(ticket, 1);
+  return __shfl_sync(0xffffffffu, item, 0);
 }
-__device__ __forceinline__ float lds_f32(uint32_t a) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
-  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
+// the last warp out resets the two ticket words for the next launch on this stream
+__device__ __forceinline__ void retire(int *ticket, int lane) {
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(ticket + 1, 1) == (int)(gridDim.x * (blockDim.x >> 5)) - 1) {
+      ticket[0] = 0;
+      ticket[1] = 0;
+    }
+  }
 }
 
-__device__ __forceinline__ void red_add_v4(float4 *addr, float4 v) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-}
-
-
-// Row-owner forward.  Each warp takes batches of 32 list entries strided over the
-// tile's list (batch j -> warp j % kFwdWarps) and stages them in smem.  Lane l owns tile
-// row q = l % T of accumulator copy l / T (32/T private copies per warp), and
-// walks the row segments AABB_k ∩ row q of the batch's entries of its copy
-// (entry k -> copy k % (32/T)) in ascending k: for one segment it evaluates
-// amp exp(-Q/2) along the row, two columns per iteration with packed fp32
-// (FFMA2).  All lanes of a round work on distinct (copy, row) accumulators, so
-// there are no write conflicts and no atomics; the per-warp copies are summed in
-// a fixed order at the end (bitwise deterministic).  Lane utilisation is the
-// fraction of rows with a segment in the round times mean/max segment width.
-constexpr int kFwdWarps = 4;
+// Forward kernel.  Register accumulators: lane L owns row pair p = L / NCP of the tile
+// (NCP = 32 / NP lanes per pair) and keeps a private copy of that pair-row, T columns x 2 rows,
+// in registers.  Per chunk of <= kCH entries, each lane takes one entry, computes its constants
+// and the start values of its row-pair segments (vertical recurrence) and appends each segment
+// to the bin of its row pair (ballots, in list order: deterministic).  Then the NCP lanes of
+// pair p take the segments of bin p round-robin and render each one with a fully unrolled,
+// predicated T-column recurrence into their registers: no shared-memory read-modify-write,
+// no divergence from box widths.  At the end the NCP copies of each pair-row are summed by a
+// fixed butterfly of shuffles (bitwise deterministic).
+template <int T>
+struct FwdSmem {
+  static constexpr int NP = T / 2;
+  float4 sA[NP][kCH];   // fast: (eA, eB, RA, RB) at column cu0; slow: (fA, fB, gA, gB)
+  float2 sB[NP][kCH];   // (S or na, bits = cu0 | cu1 << 8 | vA << 16 | vB << 17 | slow << 31)
+};
 
 template <int T>
-__global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, const SplatRec *__restrict__ rec,
+__global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, const SplatRec *__restrict__ rec,
                                                                 const int *__restrict__ base,
                                                                 const int *__restrict__ ids,
-                                                                float *__restrict__ proj) {
-  constexpr int S = T + 1;                    // accumulator row stride (floats)
-  constexpr int NCP = 32 / T;                 // accumulator copies per warp (one lane per row each)
-  constexpr int COPY = T * S;
-  __shared__ float acc[kFwdWarps][NCP * COPY];
-  __shared__ float4 st0[kFwdWarps][32];       // (bu0 - mx', my', na, nb2)  tile-local, pre-scaled conic
-  __shared__ float4 st1[kFwdWarps][32];       // (nc, amp, bu0 | w << 8, -)
-  const int t = blockIdx.x, i = blockIdx.y, tid = threadIdx.x;
-  const int lane = tid & 31, w = tid >> 5;
-  const int q = lane % T, cp = lane / T;
-  const int u0 = (t % c.nt) * T, v0 = (t / c.nt) * T;
-  const size_t hidx = ((size_t)i * c.NT + t) * c.C;
-  int s = base[hidx], e = base[hidx + c.C];
-  if ((int64_t)e > c.cap) e = (int)c.cap;
-  if ((int64_t)s > c.cap) s = (int)c.cap;
-  if (s >= e) {  // empty tile: the projection is zero there
-    for (int pp = tid; pp < T * T; pp += kFwdWarps * 32) {
-      const int u = u0 + pp % T, v = v0 + pp / T;
-      if (u < c.D && v < c.D) proj[((size_t)i * c.D + v) * c.D + u] = 0.f;
-    }
-    return;
-  }
-  for (int k = lane; k < NCP * COPY; k += 32) acc[w][k] = 0.f;
-  const SplatRec *reci = rec + (size_t)i * c.N;
-  const float nh = -0.5f * kLog2e;
-  const uint32_t rowb = smem_u32(&acc[w][cp * COPY + q * S]);
-  const unsigned csel = (NCP == 2 ? 0x55555555u : (NCP == 4 ? 0x11111111u : 0x01010101u)) << cp;
-  const float qf = (float)q;
-  __syncwarp();
-  // Batch j (j = 0 .. nbat-1, warp j % kFwdWarps) holds entries s + j + nbat * l, l = 0..31:
-  // strided over the whole (spatially ordered) list, so a batch's boxes spread over all
-  // rows of the tile and the per-row segment counts stay balanced across lanes.
-  const int nlist = e - s, nbat = (nlist + 31) >> 5;
-  int j = w;
-  SplatRec nr;
-  if (j < nbat && j + nbat * lane < nlist) nr = reci[ids[s + j + nbat * lane]];
-  for (; j < nbat; j += kFwdWarps) {
-    const bool have = j + nbat * lane < nlist;
-    const SplatRec r = nr;
-    const int jn = j + kFwdWarps;
-    if (jn < nbat && jn + nbat * lane < nlist) nr = reci[ids[s + jn + nbat * lane]];
-    int bv0 = T, bv1 = -1;
-    if (have) {
-      const int ub = __float_as_int(r.f1.z), vb = __float_as_int(r.f1.w);
-      const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
-      const int bu0 = max(ulo - u0, 0), wd = min(uhi - u0, T - 1) - bu0 + 1;
-      bv0 = max(vlo - v0, 0);
-      bv1 = min(vhi - v0, T - 1);
-      const float mx = (float)(ulo - u0) + r.f0.x, my = (float)(vlo - v0) + r.f0.y;
-      st0[w][lane] = make_float4((float)bu0 - mx, my, nh * r.f0.z, 2.f * nh * r.f0.w);
-      st1[w][lane] = make_float4(nh * r.f1.x, r.f1.y, __int_as_float(bu0 | (wd << 8)), 0.f);
-    }
-    unsigned mine = 0;   // entries of this batch whose box covers my row, of my copy
+                                                                float *__restrict__ proj, int *ticket) {
+  using SM = FwdSmem<T>;
+  constexpr int NP = T / 2, NCP = 32 / NP;
+  constexpr float nh = -0.5f * kLog2e;
+  extern __shared__ __align__(16) unsigned char fwd_dsm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  SM &sm = reinterpret_cast<SM *>(fwd_dsm)[w];
+  const unsigned lt = (1u << lane) - 1u;
+  const int mp = lane / NCP, cp = lane % NCP;
+  const int items = B * c.NT;
+  for (;;) {
+    const int item = next_item(ticket, lane);
+    if (item >= items) break;
+    const int i = item / c.NT, t = item - i * c.NT;
+    const int u0 = (t % c.nt) * T, v0 = (t / c.nt) * T;
+    const size_t hidx = ((size_t)i * c.NT + t) * c.C;
+    int s = base[hidx], e = base[hidx + c.C];
+    if ((int64_t)e > c.cap) e = (int)c.cap;
+    if ((int64_t)s > c.cap) s = (int)c.cap;
+    float *out = proj + (size_t)i * c.D * c.D;
+    float2 acc[T];
 #pragma unroll
-    for (int rr = 0; rr < T; ++rr) {
-      const unsigned m = __ballot_sync(0xffffffffu, bv0 <= rr && rr <= bv1);
-      if (rr == q) mine = m;
-    }
-    mine &= csel;
-    __syncwarp();
-#pragma unroll 1
-    while (__any_sync(0xffffffffu, mine != 0)) {
-      int wd = 0;
-      float4 E0 = make_float4(0.f, 0.f, 0.f, 0.f), E1 = E0;
-      if (mine) {
-        const int k = __ffs(mine) - 1;
-        mine &= mine - 1;
-        E0 = st0[w][k];
-        E1 = st1[w][k];
-        wd = __float_as_int(E1.z) >> 8;
+    for (int k = 0; k < T; ++k) acc[k] = make_float2(0.f, 0.f);
+    const SplatRec *reci = rec + (size_t)i * c.N;
+    for (int cs = s; cs < e; cs += kCH) {
+      const int n = min(kCH, e - cs);
+      int blen = 0;   // length of bin mp (lanes of pair pp hold bin pp's length)
+      for (int q0 = 0; q0 < n; q0 += 32) {
+        const int q = q0 + lane;
+        int pr0 = NP, pr1 = -1, cu0 = 0, cu1 = 0, cv0 = 0, cv1 = 0;
+        bool slow = false, neg = false;
+        float El = 0.f, V = 0.f, Rl = 0.f, W = 0.f, Kb = 0.f, S = 0.f, na = 0.f, nb2 = 0.f, nc = 0.f, Fx = 0.f,
+              Gx = 0.f, D0 = 0.f, my = 0.f, la = 0.f;
+        if (q < n) {
+          const SplatRec rr = reci[ids[cs + q]];
+          const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
+          const int ulo = (ub & 0xffff) - u0, uhi = (ub >> 16) - u0, vlo = (vb & 0xffff) - v0, vhi = (vb >> 16) - v0;
+          cu0 = max(ulo, 0); cu1 = min(uhi, T - 1); cv0 = max(vlo, 0); cv1 = min(vhi, T - 1);
+          pr0 = cv0 >> 1; pr1 = cv1 >> 1;
+          na = nh * rr.f0.z; nb2 = 2.f * nh * rr.f0.w; nc = nh * rr.f1.x;
+          const float mx = (float)ulo + rr.f0.x;
+          my = (float)vlo + rr.f0.y;
+          const float dx0 = (float)cu0 - mx;
+          Fx = na * dx0 * dx0; Gx = nb2 * dx0; D0 = na * fmaf(2.f, dx0, 1.f);
+          const float d0 = (float)cv0 - my, d1 = (float)cv1 - my;
+          const float f0 = fmaf(d0, fmaf(nc, d0, Gx), Fx), f1 = fmaf(d1, fmaf(nc, d1, Gx), Fx);
+          const float r0 = fmaf(nb2, d0, D0), r1 = fmaf(nb2, d1, D0);
+          slow = !(fminf(f0, f1) >= -100.f && fminf(r0, r1) >= -120.f && nc >= -60.f && fabsf(nb2) <= 120.f);
+          const float amp = rr.f1.y;
+          S = ex2(2.f * na);
+          W = ex2(2.f * nc);
+          Kb = ex2(nb2);
+          El = amp * ex2(f0);
+          V = ex2(fmaf(nc, fmaf(2.f, d0, 1.f), Gx));
+          Rl = ex2(r0);
+          la = __log2f(fabsf(amp));
+          neg = amp < 0.f;
+          if (neg) slow = true;   // the direct path carries the sign
+        }
+        const int sbits = cu0 | (cu1 << 8) | (slow ? (int)0x80000000 : 0) | (neg ? 1 << 18 : 0);
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+          const bool in = pr0 <= pp && pp <= pr1;
+          const bool vA = in && 2 * pp >= cv0, vB = in && 2 * pp + 1 <= cv1;
+          float4 sa;
+          float2 sb;
+          if (!slow) {
+            sa.x = vA ? El : 0.f;
+            sa.z = vA ? Rl : 0.f;
+            if (vA) { El *= V; V *= W; Rl *= Kb; }
+            sa.y = vB ? El : 0.f;
+            sa.w = vB ? Rl : 0.f;
+            if (vB) { El *= V; V *= W; Rl *= Kb; }
+            sb = make_float2(S, __int_as_float(sbits));
+          } else {
+            const float dA = (float)(2 * pp) - my, dB = dA + 1.f;
+            sa = make_float4(fmaf(dA, fmaf(nc, dA, Gx), Fx) + la, fmaf(dB, fmaf(nc, dB, Gx), Fx) + la,
+                             fmaf(nb2, dA, D0), fmaf(nb2, dB, D0));
+            sb = make_float2(na, __int_as_float(sbits | (vA ? 1 << 16 : 0) | (vB ? 1 << 17 : 0)));
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, in);
+          const int before = __shfl_sync(0xffffffffu, blen, pp * NCP);
+          if (in) {
+            const int pos = before + __popc(bal & lt);
+            sm.sA[pp][pos] = sa;
+            sm.sB[pp][pos] = sb;
+          }
+          if (mp == pp) blen += __popc(bal);
+        }
       }
-      const int wmax = __reduce_max_sync(0xffffffffu, wd);
-      const float dy = qf - E0.y;
-      const float t1 = E0.w * dy, t2 = E1.x * dy * dy;
-      const float2 na2 = make_float2(E0.z, E0.z), t12 = make_float2(t1, t1), t22 = make_float2(t2, t2);
-      float2 dx = make_float2(E0.x, E0.x + 1.f);
-      const uint32_t a0 = rowb + 4u * (uint32_t)(__float_as_int(E1.z) & 0xff);
-      const float amp = E1.y;
+      __syncwarp();
+      // render: lanes of pair mp take segments cp, cp + NCP, ... of bin mp
 #pragma unroll 1
-      for (int cc = 0; cc < wmax; cc += 2) {
-        const float2 arg = __ffma2_rn(__ffma2_rn(na2, dx, t12), dx, t22);
-        const float ea = ex2(arg.x), eb = ex2(arg.y);
-        const uint32_t a = a0 + 4u * (uint32_t)cc;
-        if (cc < wd) sts_f32(a, fmaf(amp, ea, lds_f32(a)));
-        if (cc + 1 < wd) sts_f32(a + 4u, fmaf(amp, eb, lds_f32(a + 4u)));
-        dx = __fadd2_rn(dx, make_float2(2.f, 2.f));
+      for (int sg = cp; __any_sync(0xffffffffu, sg < blen); sg += NCP) {
+        if (sg >= blen) continue;
+        const float4 A = sm.sA[mp][sg];
+        const float2 Bv = sm.sB[mp][sg];
+        const int bits = __float_as_int(Bv.y);
+        const int k0 = bits & 0xff, k1 = (bits >> 8) & 0xff;
+        if (bits >= 0) {
+          float2 E2 = make_float2(A.x, A.y), R2 = make_float2(A.z, A.w);
+          const float2 S2 = make_float2(Bv.x, Bv.x);
+#pragma unroll
+          for (int k = 0; k < T; ++k) {
+            if (k >= k0 && k <= k1) {
+              acc[k] = __fadd2_rn(acc[k], E2);
+              E2 = __fmul2_rn(E2, R2);
+              R2 = __fmul2_rn(R2, S2);
+            }
+          }
+        } else {   // direct evaluation: f = f0 + kk g0 + kk (kk - 1) na, kk = k - k0
+          const float sg1 = (bits & (1 << 18)) ? -1.f : 1.f;
+          const bool vA = bits & (1 << 16), vB = bits & (1 << 17);
+#pragma unroll
+          for (int k = 0; k < T; ++k) {
+            if (k >= k0 && k <= k1) {
+              const float kf = (float)(k - k0), kq = kf * (kf - 1.f) * Bv.x;
+              if (vA) acc[k].x += sg1 * ex2(fmaf(kf, A.z, A.x) + kq);
+              if (vB) acc[k].y += sg1 * ex2(fmaf(kf, A.w, A.y) + kq);
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // sum the NCP copies of each pair-row (fixed butterfly), lane cp writes columns cp, cp + NCP, ...
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+#pragma unroll
+      for (int d = 1; d < NCP; d <<= 1) {
+        acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, d);
+        acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, d);
       }
     }
-    __syncwarp();
-  }
-  __syncthreads();
-  for (int pp = tid; pp < T * T; pp += kFwdWarps * 32) {
-    const int pu = pp % T, pv = pp / T;
-    float sum = 0.f;
+    const int v = v0 + 2 * mp;
 #pragma unroll
-    for (int ww = 0; ww < kFwdWarps; ++ww)
-#pragma unroll
-      for (int k = 0; k < NCP; ++k) sum += acc[ww][k * COPY + pv * S + pu];
-    const int u = u0 + pu, v = v0 + pv;
-    if (u < c.D && v < c.D) proj[((size_t)i * c.D + v) * c.D + u] = sum;
+    for (int k = 0; k < T; ++k) {
+      if (k % NCP == cp) {
+        const int u = u0 + k;
+        if (u < c.D && v < c.D) out[(size_t)v * c.D + u] = acc[k].x;
+        if (u < c.D && v + 1 < c.D) out[(size_t)(v + 1) * c.D + u] = acc[k].y;
+      }
+    }
   }
+  retire(ticket, lane);
 }
 
-// Backward: one thread per list entry.  A warp's time is set by its largest
-// box ∩ tile, so the tile's whole list (up to kBwdMax entries per round) is first
-// counting-sorted in smem by the class (min(h,8), min(ceil(w/2),4)) of its box:
-// consecutive entries — one warp's — then have near-equal loop trip counts.
-constexpr int kBwdThreads = 256;
-constexpr int kBwdKeys = 32;
-constexpr int kBwdMax = 4096;
+// Backward ("gradient computation restricted to the Gaussians contributing to each pixel",
+// PAPER.md:108, :117), Gaussian-parallel: one thread per (particle i, Gaussian j) with a
+// non-empty AABB walks the whole box (no tiles, no lists) with the forward's recurrences,
+// two rows at a time (packed fp32), reading g = dL/dI_hat through L1/L2 (ids are in Morton
+// order, so the 32 boxes of a warp are spatial neighbours and their reads share cache lines).
+// Per row pair it accumulates packed sums of h = g e, h k, h k^2 (k = column offset), folds
+// them with dy into six moments, from which the six 2D partials (L_amp, L_mx, L_my, L_a, L_b,
+// L_c) follow algebraically and reduce to the image-space gradient (q0 = L_amp amp, l_mx,
+// l_my, G_hat 00/01/11, in Angstrom units), written to slot (i, j): one writer per slot, a
+// coalesced store, no atomics; k_bwd_reduce sums over i in a fixed order (deterministic).
+constexpr int kBwdBlock = 256;
+
+__global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, const SplatRec *__restrict__ rec,
+                                                          const float *__restrict__ dldi, float4 *__restrict__ slotA,
+                                                          float2 *__restrict__ slotB) {
+  constexpr float nh = -0.5f * kLog2e;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+  if (j >= c.N) return;
+  const size_t ij = (size_t)i * c.N + j;
+  const SplatRec rr = rec[ij];
+  const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
+  const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
+  if (ulo > uhi || vlo > vhi) {   // culled: zero slot (the reducer reads every slot)
+    slotA[ij] = make_float4(0.f, 0.f, 0.f, 0.f);
+    slotB[ij] = make_float2(0.f, 0.f);
+    return;
+  }
+  const int wd = uhi - ulo + 1, ht = vhi - vlo + 1;
+  const float ka = rr.f0.z, kb = rr.f0.w, kc = rr.f1.x, amp = rr.f1.y;
+  const float na = nh * ka, nb2 = 2.f * nh * kb, nc = nh * kc;
+  const float dx0 = -rr.f0.x, dy0 = -rr.f0.y;   // first pixel relative to the centre
+  const float Fx = na * dx0 * dx0, Gx = nb2 * dx0, D0 = na * fmaf(2.f, dx0, 1.f);
+  const float dyl = dy0 + (float)(ht - 1);
+  const float f0 = fmaf(dy0, fmaf(nc, dy0, Gx), Fx), f1 = fmaf(dyl, fmaf(nc, dyl, Gx), Fx);
+  const float r0 = fmaf(nb2, dy0, D0), r1 = fmaf(nb2, dyl, D0);
+  const bool slow = !(fminf(f0, f1) >= -100.f && fminf(r0, r1) >= -120.f && nc >= -60.f && fabsf(nb2) <= 120.f);
+  const float *gi = dldi + ((size_t)i * c.D + vlo) * c.D + ulo;
+  float M0 = 0.f, M1 = 0.f, M2 = 0.f, Y0 = 0.f, Y1 = 0.f, YY = 0.f;
+  float El = 0.f, V = 0.f, Rl = 0.f, W = 0.f, Kb = 0.f, S = 0.f;
+  if (!slow) {
+    El = ex2(f0);
+    V = ex2(fmaf(nc, fmaf(2.f, dy0, 1.f), Gx));
+    Rl = ex2(r0);
+    W = ex2(2.f * nc);
+    Kb = ex2(nb2);
+    S = ex2(2.f * na);
+  }
+  const float2 S2 = make_float2(S, S), one = make_float2(1.f, 1.f);
+#pragma unroll 1
+  for (int r2 = 0; r2 < ht; r2 += 2) {
+    const bool vB = r2 + 1 < ht;
+    const float dyA = dy0 + (float)r2, dyB = dyA + 1.f;
+    const float *ga = gi + (size_t)r2 * c.D, *gb = ga + c.D;
+    float2 T0 = make_float2(0.f, 0.f), T1 = T0, T2 = T0;
+    if (!slow) {
+      float2 E2, R2;
+      E2.x = El;
+      R2.x = Rl;
+      El *= V; V *= W; Rl *= Kb;
+      E2.y = vB ? El : 0.f;
+      R2.y = vB ? Rl : 0.f;
+      if (vB) { El *= V; V *= W; Rl *= Kb; }
+      float2 kk = make_float2(0.f, 0.f);
+#pragma unroll 2
+      for (int k = 0; k < wd; ++k) {
+        const float2 g2 = make_float2(__ldg(ga + k), vB ? __ldg(gb + k) : 0.f);
+        const float2 h = __fmul2_rn(g2, E2);
+        const float2 hk = __fmul2_rn(h, kk);
+        T0 = __fadd2_rn(T0, h);
+        T1 = __fadd2_rn(T1, hk);
+        T2 = __ffma2_rn(hk, kk, T2);
+        E2 = __fmul2_rn(E2, R2);
+        R2 = __fmul2_rn(R2, S2);
+        kk = __fadd2_rn(kk, one);
+      }
+    } else {   // direct evaluation, exp per pixel
+      const float fA = fmaf(dyA, fmaf(nc, dyA, Gx), Fx), fB = fmaf(dyB, fmaf(nc, dyB, Gx), Fx);
+      const float gA = fmaf(nb2, dyA, D0), gB = fmaf(nb2, dyB, D0);
+#pragma unroll 1
+      for (int k = 0; k < wd; ++k) {
+        const float kf = (float)k, kq = kf * (kf - 1.f) * na;
+        const float hA = __ldg(ga + k) * ex2(fmaf(kf, gA, fA) + kq);
+        const float hB = vB ? __ldg(gb + k) * ex2(fmaf(kf, gB, fB) + kq) : 0.f;
+        T0.x += hA; T0.y += hB;
+        T1.x = fmaf(hA, kf, T1.x); T1.y = fmaf(hB, kf, T1.y);
+        T2.x = fmaf(hA * kf, kf, T2.x); T2.y = fmaf(hB * kf, kf, T2.y);
+      }
+    }
+    M0 += T0.x + T0.y;
+    M1 += T1.x + T1.y;
+    M2 += T2.x + T2.y;
+    Y0 = fmaf(dyA, T0.x, fmaf(dyB, T0.y, Y0));
+    Y1 = fmaf(dyA, T1.x, fmaf(dyB, T1.y, Y1));
+    YY = fmaf(dyA * dyA, T0.x, fmaf(dyB * dyB, T0.y, YY));
+  }
+  // k-moments -> dx-moments (dx = dx0 + k)
+  const float A0 = M0, A1 = fmaf(dx0, M0, M1), A2 = fmaf(dx0, fmaf(dx0, M0, 2.f * M1), M2);
+  const float Ay0 = Y0, Ay1 = fmaf(dx0, Y0, Y1), Ayy0 = YY;
+  const float La = A0;
+  const float Lmx = amp * fmaf(ka, A1, kb * Ay0), Lmy = amp * fmaf(kb, A1, kc * Ay0);
+  const float Lpa = -0.5f * amp * A2, Lpb = -amp * Ay1, Lpc = -0.5f * amp * Ayy0;
+  // G_Sigma_hat (pixel units) = -K Gk K - 1/2 L_amp amp K, Gk = [[Lpa, Lpb/2],[Lpb/2, Lpc]]
+  const float g01 = 0.5f * Lpb;
+  const float KG00 = ka * Lpa + kb * g01, KG01 = ka * g01 + kb * Lpc;
+  const float KG10 = kb * Lpa + kc * g01, KG11 = kb * g01 + kc * Lpc;
+  const float hl = 0.5f * La * amp;
+  const float inv_px = 1.f / c.px, inv_px2 = inv_px * inv_px;
+  const float G00 = (-(KG00 * ka + KG01 * kb) - hl * ka) * inv_px2;
+  const float G01 = (-(KG00 * kb + KG01 * kc) - hl * kb) * inv_px2;
+  const float G11 = (-(KG10 * kb + KG11 * kc) - hl * kc) * inv_px2;
+  slotA[ij] = make_float4(La * amp, Lmx * inv_px, Lmy * inv_px, G00);
+  slotB[ij] = make_float2(G01, G11);
+}
+
+// Per-Gaussian reduction of the image-space slots over the particles of a launch, in a fixed
+// order (deterministic), transformed to world frame with W_i = P_i^T and added to acc:
+//   G_mu += W^T (l_mx, l_my, 0),  G_Sigma += W^T [G_hat 0; 0 0] W,  L_rho += q0 / rho.
+__global__ void __launch_bounds__(256) k_bwd_reduce(int B, int N,
+                                                    const float4 *__restrict__ slotA,
+                                                    const float2 *__restrict__ slotB,
+                                                    const float4 *__restrict__ mean_rho,
+                                                    const float *__restrict__ rot, float4 *__restrict__ acc) {
+  // thread (g, jl): Gaussian j = 64 blockIdx.x + jl, particles i = g, g + 4, ...; the four
+  // partial sums are combined in a fixed order (deterministic)
+  extern __shared__ float srot[];   // B x 6: rows 0 and 1 of W
+  __shared__ float part[3][10][64];
+  for (int k = threadIdx.x; k < 6 * B; k += blockDim.x) {
+    const int i = k / 6, e = k % 6;
+    srot[k] = rot[9 * i + 3 * (e % 3) + e / 3];   // W[row][col] = P[3 col + row], row = e / 3
+  }
+  __syncthreads();
+  const int jl = threadIdx.x & 63, g = threadIdx.x >> 6;
+  const int j = blockIdx.x * 64 + jl;
+  float v[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (j < N) {
+#pragma unroll 4
+    for (int i = g; i < B; i += 4) {
+      const size_t ij = (size_t)i * N + j;
+      const float4 sa = __ldg(&slotA[ij]);
+      const float2 sb = __ldg(&slotB[ij]);
+      const float *Wr = srot + 6 * i;
+      const float W0[3] = {Wr[0], Wr[1], Wr[2]}, W1[3] = {Wr[3], Wr[4], Wr[5]};
+      const float lmx = sa.y, lmy = sa.z, G00 = sa.w, G01 = sb.x, G11 = sb.y;
+      v[0] += sa.x;
+      v[1] += lmx * W0[0] + lmy * W1[0];
+      v[2] += lmx * W0[1] + lmy * W1[1];
+      v[3] += lmx * W0[2] + lmy * W1[2];
+      float t0[3], t1[3];
+#pragma unroll
+      for (int l = 0; l < 3; ++l) { t0[l] = G00 * W0[l] + G01 * W1[l]; t1[l] = G01 * W0[l] + G11 * W1[l]; }
+      v[4] += W0[0] * t0[0] + W1[0] * t1[0];
+      v[5] += W0[0] * t0[1] + W1[0] * t1[1];
+      v[6] += W0[0] * t0[2] + W1[0] * t1[2];
+      v[7] += W0[1] * t0[1] + W1[1] * t1[1];
+      v[8] += W0[1] * t0[2] + W1[1] * t1[2];
+      v[9] += W0[2] * t0[2] + W1[2] * t1[2];
+    }
+  }
+  if (g > 0)
+#pragma unroll
+    for (int k = 0; k < 10; ++k) part[g - 1][k][jl] = v[k];
+  __syncthreads();
+  if (g > 0 || j >= N) return;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) v[k] = ((v[k] + part[0][k][jl]) + part[1][k][jl]) + part[2][k][jl];
+  const float rho = mean_rho[j].w;
+  float4 *dst = acc + 3 * (size_t)j;
+  float4 a0 = dst[0], a1 = dst[1], a2 = dst[2];
+  a0.x += rho != 0.f ? v[0] / rho : 0.f;
+  a0.y += v[1]; a0.z += v[2]; a0.w += v[3];
+  a1.x += v[4]; a1.y += v[5]; a1.z += v[6]; a1.w += v[7];
+  a2.x += v[8]; a2.y += v[9];
+  dst[0] = a0; dst[1] = a1; dst[2] = a2;
+}
+
+template <typename K>
+int persistent_grid(K kern, int threads, size_t smem) {
+  int dev = 0, sms = 0, b = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem);
+  return sms * (b > 0 ? b : 1);
+}
 
 template <int T>
-__global__ void __launch_bounds__(kBwdThreads) k_render_bwd(CfgDev c, const SplatRec *__restrict__ rec,
-                                                             const uint2 *__restrict__ box,
-                                                             const int *__restrict__ base, const int *__restrict__ ids,
-                                                             const float *__restrict__ dldi,
-                                                             const float4 *__restrict__ mean_rho,
-                                                             const float *__restrict__ rot, float4 *__restrict__ acc) {
-  __shared__ float gs[T + 1][T + 1];   // one spare row: the paired loop may read one past a row
-  __shared__ unsigned char skey[kBwdMax];
-  __shared__ unsigned short order[kBwdMax];
-  __shared__ int hist[kBwdKeys];
-  const int t = blockIdx.x, i = blockIdx.y, tid = threadIdx.x;
-  const int u0 = (t % c.nt) * T, v0 = (t / c.nt) * T;
-  const size_t hidx = ((size_t)i * c.NT + t) * c.C;
-  int s = base[hidx], e = base[hidx + c.C];
-  if ((int64_t)e > c.cap) e = (int)c.cap;
-  if ((int64_t)s > c.cap) s = (int)c.cap;
-  if (s >= e) return;  // empty tile: no Gaussian touches it
-  for (int pp = tid; pp < T * T; pp += kBwdThreads) {
-    const int pu = pp % T, pv = pp / T, u = u0 + pu, v = v0 + pv;
-    gs[pv][pu] = (u < c.D && v < c.D) ? dldi[((size_t)i * c.D + v) * c.D + u] : 0.f;
-  }
-  // W = P^T: W[r][k] = P[3k + r]; only rows 0 and 1 of W are needed.
-  float W0[3], W1[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    W0[k] = rot[9 * i + 3 * k];
-    W1[k] = rot[9 * i + 3 * k + 1];
-  }
-  const float inv_px = 1.f / c.px, inv_px2 = inv_px * inv_px;
-  const float nh = -0.5f * kLog2e;
-  const SplatRec *reci = rec + (size_t)i * c.N;
-  const uint2 *boxi = box + (size_t)i * c.N;
-  for (int cs = s; cs < e; cs += kBwdMax) {
-    const int n = min(kBwdMax, e - cs);
-    if (tid < kBwdKeys) hist[tid] = 0;
-    __syncthreads();
-    for (int k = tid; k < n; k += kBwdThreads) {
-      const uint2 b = boxi[ids[cs + k]];
-      const int wd = min((int)(b.x >> 16), u0 + T - 1) - max((int)(b.x & 0xffff), u0) + 1;
-      const int ht = min((int)(b.y >> 16), v0 + T - 1) - max((int)(b.y & 0xffff), v0) + 1;
-      const int key = (min(ht, 8) - 1) * 4 + min((wd + 1) >> 1, 4) - 1;
-      skey[k] = (unsigned char)key;
-      atomicAdd(&hist[key], 1);
-    }
-    __syncthreads();
-    if (tid < 32) {   // exclusive scan of the 32 class counts
-      const int hv = hist[tid];
-      int incl = hv;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, d);
-        if (tid >= d) incl += y;
-      }
-      hist[tid] = incl - hv;
-    }
-    __syncthreads();
-    for (int k = tid; k < n; k += kBwdThreads) order[atomicAdd(&hist[skey[k]], 1)] = (unsigned short)k;
-    __syncthreads();
-    for (int kk = tid; kk < n; kk += kBwdThreads) {
-      const int id = ids[cs + order[kk]];
-      const SplatRec r = reci[id];
-      const int ub = __float_as_int(r.f1.z), vb = __float_as_int(r.f1.w);
-      const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
-      const float mxr = r.f0.x, myr = r.f0.y, a = r.f0.z, b = r.f0.w, cc = r.f1.x, amp = r.f1.y;
-    const int ua = max(ulo, u0), ubnd = min(uhi, u0 + T - 1), va = max(vlo, v0), vbnd = min(vhi, v0 + T - 1);
-    // Per row (dy fixed) accumulate T0 = sum g e, T1 = sum g e dx, T2 = sum g e dx^2; since
-    // h = amp g e, the six partials are L_amp = sum T0 and, over rows,
-    // L_mx = amp (a sum T1 + b sum dy T0), L_my = amp (b sum T1 + c sum dy T0),
-    // L_a = -amp/2 sum T2, L_b = -amp sum dy T1, L_c = -amp/2 sum dy^2 T0.
-    const float na = nh * a, nb2 = 2.f * nh * b, nc = nh * cc;
-    float A0 = 0.f, A1 = 0.f, A2 = 0.f, Ay0 = 0.f, Ay1 = 0.f, Ayy0 = 0.f;
-    const float dx0 = (float)(ua - ulo) - mxr;
-    float dy = (float)(va - vlo) - myr;
-    const float *grow = &gs[va - v0][ua - u0];
-    const int nu = ubnd - ua;                 // row length - 1
-    const float2 na2 = make_float2(na, na), two = make_float2(2.f, 2.f);
-#pragma unroll 1
-    for (int v = va; v <= vbnd; ++v, dy += 1.f, grow += T + 1) {
-      const float t1 = nb2 * dy, t2 = nc * dy * dy;
-      const float2 t12 = make_float2(t1, t1), t22 = make_float2(t2, t2);
-      float2 dx = make_float2(dx0, dx0 + 1.f);
-      float2 T0 = make_float2(0.f, 0.f), T1 = T0, T2 = T0;
-      const float *gp = grow;
-#pragma unroll 1
-      for (int uu = 0; uu <= nu; uu += 2, gp += 2) {   // two pixels per iteration (FFMA2)
-        const float2 arg = __ffma2_rn(__ffma2_rn(na2, dx, t12), dx, t22);
-        const float2 g2 = make_float2(gp[0], uu < nu ? gp[1] : 0.f);
-        const float2 ge = __fmul2_rn(g2, make_float2(ex2(arg.x), ex2(arg.y)));
-        const float2 gdx = __fmul2_rn(ge, dx);
-        T0 = __fadd2_rn(T0, ge);
-        T1 = __fadd2_rn(T1, gdx);
-        T2 = __ffma2_rn(gdx, dx, T2);
-        dx = __fadd2_rn(dx, two);
-      }
-      const float s0 = T0.x + T0.y, s1 = T1.x + T1.y, s2 = T2.x + T2.y;
-      A0 += s0;
-      A1 += s1;
-      A2 += s2;
-      Ay0 = fmaf(dy, s0, Ay0);
-      Ay1 = fmaf(dy, s1, Ay1);
-      Ayy0 = fmaf(dy * dy, s0, Ayy0);
-    }
-    const float La = A0;
-    const float Lmx = amp * fmaf(a, A1, b * Ay0), Lmy = amp * fmaf(b, A1, cc * Ay0);
-    float Lpa = amp * A2, Lpb = amp * Ay1, Lpc = amp * Ayy0;
-    Lpa *= -0.5f; Lpb = -Lpb; Lpc *= -0.5f;
-    // G_Sigma_hat (pixel units) = -K Gk K - 1/2 L_amp amp K, Gk = [[Lpa, Lpb/2],[Lpb/2, Lpc]]
-    const float g01 = 0.5f * Lpb;
-    const float KG00 = a * Lpa + b * g01, KG01 = a * g01 + b * Lpc;
-    const float KG10 = b * Lpa + cc * g01, KG11 = b * g01 + cc * Lpc;
-    const float hl = 0.5f * La * amp;
-    float G00 = -(KG00 * a + KG01 * b) - hl * a;
-    float G01 = -(KG00 * b + KG01 * cc) - hl * b;
-    float G11 = -(KG10 * b + KG11 * cc) - hl * cc;
-    G00 *= inv_px2; G01 *= inv_px2; G11 *= inv_px2;   // -> Angstrom units
-    const float lmx = Lmx * inv_px, lmy = Lmy * inv_px;
-    const float rho = mean_rho[id].w;
-    float4 o0, o1, o2;
-    o0.x = La * (amp / rho);
-    o0.y = lmx * W0[0] + lmy * W1[0];
-    o0.z = lmx * W0[1] + lmy * W1[1];
-    o0.w = lmx * W0[2] + lmy * W1[2];
-    // G_Sigma_kl = sum_ab W[a][k] G[a][b] W[b][l]
-    float M[3][3];
-#pragma unroll
-    for (int kk = 0; kk < 3; ++kk)
-#pragma unroll
-      for (int ll = kk; ll < 3; ++ll)
-        M[kk][ll] = W0[kk] * (G00 * W0[ll] + G01 * W1[ll]) + W1[kk] * (G01 * W0[ll] + G11 * W1[ll]);
-    o1 = make_float4(M[0][0], M[0][1], M[0][2], M[1][1]);
-    o2 = make_float4(M[1][2], M[2][2], 0.f, 0.f);
-    float4 *dst = acc + 3 * (size_t)id;
-    red_add_v4(dst, o0);
-    red_add_v4(dst + 1, o1);
-    red_add_v4(dst + 2, o2);
-    }
-    __syncthreads();
-  }
+void launch_fwd_t(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
+                  int *ticket, cudaStream_t s) {
+  static int grid = 0;
+  const size_t smem = sizeof(FwdSmem<T>) * kFwdWarps;
+  if (!grid) grid = persistent_grid(k_render_fwd<T>, kFwdWarps * 32, smem);
+  k_render_fwd<T><<<grid, kFwdWarps * 32, smem, s>>>(c, B, rec, base, ids, proj, ticket);
 }
 
 }  // namespace
 
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
-                       cudaStream_t s, int &launches) {
-  dim3 grid(c.NT, B);
-  if (c.T == 16) k_render_fwd<16><<<grid, kFwdWarps * 32, 0, s>>>(c, rec, base, ids, proj);
-  else k_render_fwd<8><<<grid, kFwdWarps * 32, 0, s>>>(c, rec, base, ids, proj);
+                       int *ticket, cudaStream_t s, int &launches) {
+  if (c.T == 16) launch_fwd_t<16>(c, B, rec, base, ids, proj, ticket, s);
+  else launch_fwd_t<8>(c, B, rec, base, ids, proj, ticket, s);
   ++launches;
 }
 
-void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const uint2 *box, const int *base, const int *ids,
-                       const float *dldi, const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s,
-                       int &launches) {
-  dim3 grid(c.NT, B);
-  if (c.T == 16) k_render_bwd<16><<<grid, kBwdThreads, 0, s>>>(c, rec, box, base, ids, dldi, mean_rho, rot, acc);
-  else k_render_bwd<8><<<grid, kBwdThreads, 0, s>>>(c, rec, box, base, ids, dldi, mean_rho, rot, acc);
+void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float *dldi, float4 *slotA, float2 *slotB,
+                       cudaStream_t s, int &launches) {
+  dim3 grid((c.N + kBwdBlock - 1) / kBwdBlock, B);
+  k_render_bwd<<<grid, kBwdBlock, 0, s>>>(c, rec, dldi, slotA, slotB);
+  ++launches;
+}
+
+void launch_bwd_reduce(const CfgDev &c, int B, const float4 *slotA, const float2 *slotB,
+                       const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s, int &launches) {
+  k_bwd_reduce<<<(c.N + 63) / 64, 256, sizeof(float) * 6 * B, s>>>(B, c.N, slotA, slotB, mean_rho, rot, acc);
   ++launches;
 }
 

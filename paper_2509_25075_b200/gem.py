@@ -23,7 +23,7 @@ class GemConfig:
     max_batch: int
     cull_k: float = 3.0
     tau: float = 0.0
-    tile: int = 16
+    tile: int = 8
     list_capacity: int = 0
     lr_mean: float = 1e-3
     lr_log_scale: float = 5e-3

@@ -100,6 +100,144 @@ __global__ void k_red1(float *acc, int n, int iters, unsigned seed) {
   }
 }
 
+
+__global__ void k_fmul2(float *out, int iters) {
+  float2 a = make_float2(threadIdx.x * 1e-3f, 1.f), b = make_float2(1.0001f, 0.9999f), d = a, e = a, f = a, g = a, h = a;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      a = __fmul2_rn(a, b); d = __fmul2_rn(d, b); e = __fmul2_rn(e, b); f = __fmul2_rn(f, b);
+      g = __fmul2_rn(g, b); h = __fmul2_rn(h, b);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a.x + d.x + e.x + f.x + g.x + h.x + a.y + d.y + e.y + f.y + g.y + h.y;
+}
+
+__global__ void k_ffma2(float *out, int iters) {
+  float2 a = make_float2(threadIdx.x * 1e-3f, 1.f), b = make_float2(1.0001f, 0.9999f), c = make_float2(0.5f, 0.25f);
+  float2 d = a, e = a, f = a, g = a, h = a;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      a = __ffma2_rn(a, b, c); d = __ffma2_rn(d, b, c); e = __ffma2_rn(e, b, c); f = __ffma2_rn(f, b, c);
+      g = __ffma2_rn(g, b, c); h = __ffma2_rn(h, b, c);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a.x + d.x + e.x + f.x + g.x + h.x + a.y + d.y + e.y + f.y + g.y + h.y;
+}
+
+__global__ void k_fmul(float *out, int iters) {
+  float a = threadIdx.x * 1e-3f, b = 1.0001f, d = a + 1, e = a + 2, f = a + 3, g = a + 4, h = a + 5;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      a *= b; d *= b; e *= b; f *= b; g *= b; h *= b;
+      asm volatile("" : "+f"(a), "+f"(d), "+f"(e), "+f"(f), "+f"(g), "+f"(h));
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a + d + e + f + g + h;
+}
+
+// packed recurrence RMW: per step LDS.64, FADD2, STS.64, FMUL2 x2 (two pixels)
+__global__ void k_rec_rmw(float *out, int iters) {
+  __shared__ float2 s[8][32 * 9];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = lane; t < 32 * 9; t += 32) s[w][t] = make_float2(0.f, 0.f);
+  __syncwarp();
+  float2 E = make_float2(1e-3f * lane, 2e-3f), R = make_float2(0.999f, 0.998f), S = make_float2(0.9999f, 0.9999f);
+  float2 *row = &s[w][lane * 9];
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float2 a = row[k];
+      a = __fadd2_rn(a, E);
+      row[k] = a;
+      E = __fmul2_rn(E, R);
+      R = __fmul2_rn(R, S);
+    }
+  }
+  __syncwarp();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s[w][lane].x;
+}
+
+// direct evaluation RMW: per pixel 2 FFMA, MUFU.EX2, LDS, FFMA, STS
+__global__ void k_ex2_rmw(float *out, int iters) {
+  __shared__ float s[8][32 * 17];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = lane; t < 32 * 17; t += 32) s[w][t] = 0.f;
+  __syncwarp();
+  float na = -0.7f, t1 = 0.01f * lane, t2 = -0.3f, amp = 1.3f;
+  float *row = &s[w][lane * 17];
+  for (int i = 0; i < iters; ++i) {
+    float dx = -4.f + 1e-3f * i;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float arg = fmaf(fmaf(na, dx, t1), dx, t2), e;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(arg));
+      row[k] = fmaf(amp, e, row[k]);
+      dx += 1.f;
+    }
+  }
+  __syncwarp();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s[w][lane];
+}
+
+
+// smem integer atomics with data-dependent values and scattered addresses (fixed-point accumulation)
+__global__ void k_atoms_add32(int *out, int iters) {
+  __shared__ int s[4096];
+  for (int t = threadIdx.x; t < 4096; t += blockDim.x) s[t] = 0;
+  __syncthreads();
+  unsigned x = threadIdx.x * 2654435761u;
+  int v = threadIdx.x;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      x = x * 1664525u + 1013904223u;
+      atomicAdd(&s[x >> 20], v);
+      v += k;
+    }
+  }
+  __syncthreads();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s[threadIdx.x];
+}
+__global__ void k_atoms_add64(unsigned long long *out, int iters) {
+  __shared__ unsigned long long s[2048];
+  for (int t = threadIdx.x; t < 2048; t += blockDim.x) s[t] = 0;
+  __syncthreads();
+  unsigned x = threadIdx.x * 2654435761u;
+  unsigned long long v = threadIdx.x;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      x = x * 1664525u + 1013904223u;
+      atomicAdd(&s[x >> 21], v);
+      v += k;
+    }
+  }
+  __syncthreads();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s[threadIdx.x];
+}
+// float -> int32 fixed point via magic-constant add, then ATOMS.ADD
+__global__ void k_fix_atoms(int *out, int iters) {
+  __shared__ int s[4096];
+  for (int t = threadIdx.x; t < 4096; t += blockDim.x) s[t] = 0;
+  __syncthreads();
+  unsigned x = threadIdx.x * 2654435761u;
+  float e = 0.37f + threadIdx.x * 1e-4f, r = 0.999f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      x = x * 1664525u + 1013904223u;
+      const int q = __float2int_rn(e * 1048576.f);
+      atomicAdd(&s[x >> 20], q);
+      e *= r;
+    }
+  }
+  __syncthreads();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s[threadIdx.x];
+}
+
 template <typename F>
 float timeit(F f) {
   cudaEvent_t a, b;
@@ -152,6 +290,24 @@ int main() {
   printf("red.global.add.v4.f32 random over %d float4: %.3f G ops/s\n", n, nthr * 200 / ms / 1e6);
   ms = timeit([&] { k_red1<<<blocks, threads>>>((float *)acc, 4 * n, 200, 7); });
   printf("red.global.add.f32 random over %d floats: %.3f G ops/s\n", 4 * n, nthr * 200 / ms / 1e6);
+  ms = timeit([&] { k_fmul2<<<blocks, threads>>>(buf, it); });
+  printf("FMUL2: %.2f T lane-FMUL/s (x2 packed)\n", 2 * nthr * it * 16 * 6 / ms / 1e9);
+  ms = timeit([&] { k_ffma2<<<blocks, threads>>>(buf, it); });
+  printf("FFMA2: %.2f T lane-FMA/s (x2 packed)\n", 2 * nthr * it * 16 * 6 / ms / 1e9);
+  ms = timeit([&] { k_fmul<<<blocks, threads>>>(buf, it); });
+  printf("FMUL: %.2f T lane-FMUL/s\n", nthr * it * 16 * 6 / ms / 1e9);
+  ms = timeit([&] { k_rec_rmw<<<blocks, threads>>>(buf, it / 4); });
+  printf("recurrence RMW: %.3f T pixel/s (%.2f pixels/clk/SM)\n", 2 * nthr * (it / 4) * 8 / ms / 1e9,
+         2 * nthr * (it / 4) * 8 / (ms * 1e-3) / sms / (clk * 1e3));
+  ms = timeit([&] { k_ex2_rmw<<<blocks, threads>>>(buf, it / 4); });
+  printf("ex2 RMW: %.3f T pixel/s (%.2f pixels/clk/SM)\n", nthr * (it / 4) * 16 / ms / 1e9,
+         nthr * (it / 4) * 16 / (ms * 1e-3) / sms / (clk * 1e3));
+  ms = timeit([&] { k_atoms_add32<<<blocks, threads>>>(ibuf, it / 4); });
+  printf("ATOMS.ADD.32 random: %.2f lanes/clk/SM\n", nthr * (it / 4) * 8 / (ms * 1e-3) / sms / (clk * 1e3));
+  ms = timeit([&] { k_atoms_add64<<<blocks, threads>>>((unsigned long long *)dbuf, it / 4); });
+  printf("ATOMS.ADD.64 random: %.2f lanes/clk/SM\n", nthr * (it / 4) * 8 / (ms * 1e-3) / sms / (clk * 1e3));
+  ms = timeit([&] { k_fix_atoms<<<blocks, threads>>>(ibuf, it / 4); });
+  printf("F2I + ATOMS.ADD.32 random: %.2f lanes/clk/SM\n", nthr * (it / 4) * 8 / (ms * 1e-3) / sms / (clk * 1e3));
   printf("done\n");
   return 0;
 }
