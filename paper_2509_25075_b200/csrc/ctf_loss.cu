@@ -37,31 +37,36 @@ __device__ __forceinline__ float ctf_raw(const CtfP &p, double fx, double fy) {
   return -env * (p.alpha_s * sn + p.alpha_c * cs);
 }
 
-__global__ void __launch_bounds__(kCtfThreads) k_ctf_loss(CfgDev c, const float *__restrict__ ctf,
+// Per-particle CTF constants (fp64: wavelength, defocus, Cs, astigmatism), once per particle.
+__global__ void k_ctf_params(int B, const float *__restrict__ ctf, CtfP *__restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  const float *q = ctf + 8 * i;
+  const double kV = q[3], V = kV * 1000.0;
+  const double h = 6.62607015e-34, m0 = 9.1093837015e-31, e = 1.602176634e-19, cl = 299792458.0;
+  const double lam = h / sqrt(2.0 * m0 * e * V * (1.0 + e * V / (2.0 * m0 * cl * cl))) * 1e10;
+  const double du = q[0], dv = q[1];
+  CtfP P;
+  P.K1s = kPi * lam * 0.5 * (du + dv);
+  P.K1d = kPi * lam * 0.5 * (du - dv);
+  P.K2 = 0.5 * kPi * ((double)q[4] * 1e7) * lam * lam * lam;
+  P.c2 = cos(2.0 * (double)q[2]);
+  P.s2a = sin(2.0 * (double)q[2]);
+  P.phi = q[6];
+  const double al = q[5];
+  P.alpha_s = (float)sqrt(1.0 - al * al);
+  P.alpha_c = (float)al;
+  P.bq = 0.25f * q[7];
+  out[i] = P;
+}
+
+__global__ void __launch_bounds__(kCtfThreads) k_ctf_loss(CfgDev c, const CtfP *__restrict__ ctfp,
                                                           float2 *__restrict__ spec_hat,
                                                           const float2 *__restrict__ spec_obs,
                                                           float2 *__restrict__ spec_pred, double *__restrict__ part) {
-  __shared__ CtfP P;
   __shared__ double red[kCtfThreads / 32];
   const int i = blockIdx.y, tid = threadIdx.x;
-  if (tid == 0) {
-    const float *q = ctf + 8 * i;
-    const double kV = q[3], V = kV * 1000.0;
-    const double h = 6.62607015e-34, m0 = 9.1093837015e-31, e = 1.602176634e-19, cl = 299792458.0;
-    const double lam = h / sqrt(2.0 * m0 * e * V * (1.0 + e * V / (2.0 * m0 * cl * cl))) * 1e10;
-    const double du = q[0], dv = q[1];
-    P.K1s = kPi * lam * 0.5 * (du + dv);
-    P.K1d = kPi * lam * 0.5 * (du - dv);
-    P.K2 = 0.5 * kPi * ((double)q[4] * 1e7) * lam * lam * lam;
-    P.c2 = cos(2.0 * (double)q[2]);
-    P.s2a = sin(2.0 * (double)q[2]);
-    P.phi = q[6];
-    const double al = q[5];
-    P.alpha_s = (float)sqrt(1.0 - al * al);
-    P.alpha_c = (float)al;
-    P.bq = 0.25f * q[7];
-  }
-  __syncthreads();
+  const CtfP P = ctfp[i];
   const int D = c.D, Hx = D / 2 + 1;
   const int H = D * Hx;
   const int idx = blockIdx.x * kCtfThreads + tid;
@@ -101,45 +106,56 @@ __global__ void __launch_bounds__(kCtfThreads) k_ctf_loss(CfgDev c, const float 
   }
 }
 
-// Deterministic reduction of the per-block partials: one warp per particle
-// (lane-strided sums, fixed xor tree), then warp 0 sums the particles in order.
-__global__ void __launch_bounds__(1024) k_loss_reduce(int B, int nblk, const double *__restrict__ part,
-                                                      double *__restrict__ loss, DevStats *st) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = w; i < B; i += nw) {
-    double s = 0.0;
-    for (int b = lane; b < nblk; b += 32) s += part[(size_t)i * nblk + b];
+// Deterministic reduction of the per-block partials: block i sums particle i's partials with a
+// fixed tree; the last block to finish (ticket) sums the B particle losses in order.
+__global__ void __launch_bounds__(128) k_loss_reduce(int B, int nblk, const double *__restrict__ part,
+                                                     double *__restrict__ loss, DevStats *st, int *ticket) {
+  __shared__ double red[4];
+  __shared__ int last;
+  const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  double s = 0.0;
+  for (int b = tid; b < nblk; b += 128) s += part[(size_t)i * nblk + b];
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
-    if (lane == 0) loss[i] = s;
+  for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+  if (lane == 0) red[w] = s;
+  __syncthreads();
+  if (tid == 0) {
+    loss[i] = ((red[0] + red[1]) + red[2]) + red[3];
+    __threadfence();
+    last = atomicAdd(ticket, 1) == B - 1;
   }
   __syncthreads();
-  if (w == 0) {
-    double s = 0.0;
-    for (int i = lane; i < B; i += 32) s += loss[i];
+  if (!last || w != 0) return;
+  __threadfence();
+  double t = 0.0;
+  for (int k = lane; k < B; k += 32) t += ((volatile double *)loss)[k];
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
-    if (lane == 0) {
-      loss[B] = s;
-      if (!isfinite(s)) st->nonfinite = 1;
-    }
+  for (int d = 16; d >= 1; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+  if (lane == 0) {
+    loss[B] = t;
+    if (!isfinite(t)) st->nonfinite = 1;
+    *ticket = 0;   // self-reset for the next launch on this stream
   }
 }
 
 }  // namespace
 
-void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, float2 *spec_hat, const float2 *spec_obs,
+void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
                      float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches) {
+  CtfP *P = reinterpret_cast<CtfP *>(ctf_par);
+  k_ctf_params<<<(B + 127) / 128, 128, 0, s>>>(B, ctf, P);
   dim3 grid(loss_blocks, B);
-  k_ctf_loss<<<grid, kCtfThreads, 0, s>>>(c, ctf, spec_hat, spec_obs, spec_pred, loss_part);
+  k_ctf_loss<<<grid, kCtfThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part);
+  launches += 2;
+}
+
+void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, int *ticket,
+                        cudaStream_t s, int &launches) {
+  k_loss_reduce<<<B, 128, 0, s>>>(B, loss_blocks, loss_part, loss, st, ticket);
   ++launches;
 }
 
-void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
-                        int &launches) {
-  k_loss_reduce<<<1, 1024, 0, s>>>(B, loss_blocks, loss_part, loss, st);
-  ++launches;
-}
+size_t ctf_par_bytes() { return sizeof(CtfP); }
 
 int ctf_loss_blocks(int D) { return (D * (D / 2 + 1) + kCtfThreads - 1) / kCtfThreads; }
 

@@ -77,7 +77,7 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.cufft_bytes = cufft_bytes;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
-  L.prep = take(sizeof(GaussPrep) * N);
+  L.prep = take((sizeof(GaussPrep) + sizeof(GaussPrep32)) * N);   // fp64 prep, then fp32 prep
   L.rec = take(sizeof(SplatRec) * W * N);
   L.box = take(sizeof(uint2) * W * N);
   L.hist = take(sizeof(int) * (size_t)L.n_hist);
@@ -93,6 +93,7 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.slot_b = take(sizeof(float2) * W * N);
   L.acc = take(sizeof(float4) * 3 * N);
   L.loss_part = take(sizeof(double) * Bm * (size_t)L.loss_blocks);
+  L.ctf_par = take(ctf_par_bytes() * Bm);
   L.stats = take(sizeof(DevStats));
   L.ticket = take(64);   // persistent-kernel work tickets (self-resetting; zeroed at init)
   L.stage_rot = take(sizeof(float) * 9 * Bm);
@@ -370,7 +371,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     }
     {
       Prof p(ctx, s, P_CTF_LOSS);
-      launch_ctf_loss(c, nb, ctf + 8 * (size_t)p0, sh, so, pred_out ? sp : nullptr, lpart + (size_t)p0 * L.loss_blocks,
+      launch_ctf_loss(c, nb, ctf + 8 * (size_t)p0, ctx->ws + L.ctf_par, sh, so, pred_out ? sp : nullptr, lpart + (size_t)p0 * L.loss_blocks,
                       L.loss_blocks, s, ctx->launches);
     }
     {
@@ -391,7 +392,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
   ctx->last_p0 = p0 - ctx->W;
   ctx->last_nb = nb;
   double *lossd = host ? at<double>(ctx, L.stage_loss) : loss;
-  { Prof p(ctx, s, P_CTF_LOSS); launch_loss_reduce(B, lpart, L.loss_blocks, lossd, st, s, ctx->launches); }
+  { Prof p(ctx, s, P_CTF_LOSS); launch_loss_reduce(B, lpart, L.loss_blocks, lossd, st, at<int>(ctx, L.ticket) + 4, s, ctx->launches); }
   if (host) CK(cudaMemcpyAsync(loss, lossd, sizeof(double) * (B + 1), cudaMemcpyDeviceToHost, s));
   CK(cudaGetLastError());
   ctx->fwd_live = 1;

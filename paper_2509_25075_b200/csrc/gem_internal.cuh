@@ -10,7 +10,7 @@
 
 namespace gem {
 
-constexpr int kChunk = 1024;          // Gaussians per binning chunk (a3)
+constexpr int kChunk = 4096;          // Gaussians per binning chunk (a3)
 constexpr double kSqrt2Pi = 2.5066282746310002;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -23,6 +23,12 @@ struct __align__(16) GaussPrep {
   double pad;
 };
 
+// a1 output, fp32 rotated frame for the splat fast path (48 B): column k of R(q_hat) and
+// s_k = sigma_k^2; c[0].w < 0 marks a degenerate Gaussian.
+struct __align__(16) GaussPrep32 {
+  float4 c[3];
+};
+
 // a2 output per (particle, Gaussian): splat in pixel units (32 B, two float4).
 //   f0 = (mxr, myr, a, b)   mxr = m_x/px + D/2 - u_lo (centre relative to the box corner)
 //   f1 = (c, amp, ub, vb)   ub = u_lo | u_hi << 16, vb likewise (empty box: lo > hi)
@@ -32,7 +38,7 @@ struct __align__(16) SplatRec {
 };
 
 struct Layout {  // byte offsets into the caller's workspace
-  size_t prep, rec, box, hist, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slot_a, slot_b, acc, loss_part,
+  size_t prep, rec, box, hist, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slot_a, slot_b, acc, loss_part, ctf_par,
       stats, ticket, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, total;
   int64_t n_hist;       // B_max * NT * C
   int64_t n_scan_blk;
@@ -101,9 +107,11 @@ void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, Dev
 void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, int *ids, cudaStream_t s, int &launches);
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
                        int *ticket, cudaStream_t s, int &launches);
-void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, float2 *spec_hat, const float2 *spec_obs,
+void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
                      float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches);
-void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, cudaStream_t s,
+size_t ctf_par_bytes();
+void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, int *ticket,
+                        cudaStream_t s,
                         int &launches);
 int ctf_loss_blocks(int D);
 void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float *dldi, float4 *slotA, float2 *slotB,

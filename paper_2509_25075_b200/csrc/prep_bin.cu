@@ -13,6 +13,13 @@
 namespace gem {
 namespace {
 
+// MUFU.RSQ (rel. error < 2^-22): bound error ~1e-6 px, far inside the 1e-3 px exactness margin
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsb(double a, double b) { return __dsub_rn(a, b); }
@@ -64,6 +71,23 @@ __global__ void __launch_bounds__(256) k_prep(int N, const float4 *__restrict__ 
   }
   p.ok = ok ? 1.0 : 0.0;
   prep[j] = p;
+  // fp32 rotated frame (splat fast path)
+  GaussPrep32 f;
+  if (ok) {
+    const float fw = qq.x, fx = qq.y, fy = qq.z, fz = qq.w;
+    const float inv = rsqrtf(((fw * fw + fx * fx) + fy * fy) + fz * fz);
+    const float w2 = fw * inv, x2 = fx * inv, y2 = fy * inv, z2 = fz * inv;
+    const float Rf[9] = {1.f - 2.f * (y2 * y2 + z2 * z2), 2.f * (x2 * y2 - w2 * z2), 2.f * (x2 * z2 + w2 * y2),
+                         2.f * (x2 * y2 + w2 * z2), 1.f - 2.f * (x2 * x2 + z2 * z2), 2.f * (y2 * z2 - w2 * x2),
+                         2.f * (x2 * z2 - w2 * y2), 2.f * (y2 * z2 + w2 * x2), 1.f - 2.f * (x2 * x2 + y2 * y2)};
+    const float sk[3] = {expf(2.f * ss.x), expf(2.f * ss.y), expf(2.f * ss.z)};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) f.c[k] = make_float4(Rf[k], Rf[3 + k], Rf[6 + k], sk[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) f.c[k] = make_float4(0.f, 0.f, 0.f, -1.f);
+  }
+  reinterpret_cast<GaussPrep32 *>(prep + N)[j] = f;
 }
 
 __device__ __forceinline__ int clip_d(double v, int lo, int hi) {
@@ -85,79 +109,129 @@ __global__ void __launch_bounds__(256) k_splat_count(CfgDev c, const GaussPrep *
                                                      DevStats *__restrict__ st) {
   extern __shared__ int shist[];
   const int i = blockIdx.y, ch = blockIdx.x, tid = threadIdx.x;
+  const GaussPrep32 *__restrict__ prep32 = reinterpret_cast<const GaussPrep32 *>(prep + c.N);
   for (int t = tid; t < c.NT; t += blockDim.x) shist[t] = 0;
   double W[9];
+  float Wf[6];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) W[3 * r + cc] = (double)rot[9 * i + 3 * cc + r];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) Wf[k] = (float)W[k];
   const double tx = shift[2 * i], ty = shift[2 * i + 1];
   const double px = c.px, half = (double)(c.D / 2), kk = c.k, tau = c.tau, ipx = 1.0 / px;
+  const float kf = c.k, ipxf = (float)ipx, halff = (float)half, px2f = c.px * c.px;
   unsigned long long pairs = 0;
   __syncthreads();
   for (int r = 0; r < kChunk / 256; ++r) {
     int j = ch * kChunk + r * 256 + tid;
     if (j >= c.N) break;
-    const GaussPrep g = prep[j];
     const float4 m4 = mr[j];
+    const GaussPrep32 g32 = prep32[j];
+    // centre in fp64 (the record stores it relative to the box corner to ~1e-7 px)
     const double mu0 = m4.x, mu1 = m4.y, mu2 = m4.z, rho = m4.w;
-    double mx = da(da(da(dm(W[0], mu0), dm(W[1], mu1)), dm(W[2], mu2)), tx);
-    double my = da(da(da(dm(W[3], mu0), dm(W[4], mu1)), dm(W[5], mu2)), ty);
-    // Sigma row k as S(k,l)
-    const double S00 = g.sig[0], S01 = g.sig[1], S02 = g.sig[2], S11 = g.sig[3], S12 = g.sig[4], S22 = g.sig[5];
-    double v00 = da(da(dm(S00, W[0]), dm(S01, W[1])), dm(S02, W[2]));
-    double v01 = da(da(dm(S01, W[0]), dm(S11, W[1])), dm(S12, W[2]));
-    double v02 = da(da(dm(S02, W[0]), dm(S12, W[1])), dm(S22, W[2]));
-    double v10 = da(da(dm(S00, W[3]), dm(S01, W[4])), dm(S02, W[5]));
-    double v11 = da(da(dm(S01, W[3]), dm(S11, W[4])), dm(S12, W[5]));
-    double v12 = da(da(dm(S02, W[3]), dm(S12, W[4])), dm(S22, W[5]));
-    double A = da(da(dm(W[0], v00), dm(W[1], v01)), dm(W[2], v02));
-    double Bc = da(da(dm(W[0], v10), dm(W[1], v11)), dm(W[2], v12));
-    double Cc = da(da(dm(W[3], v10), dm(W[4], v11)), dm(W[5], v12));
-    double det2 = dsb(dm(A, Cc), dm(Bc, Bc));
-    // Fast path: bounds with a multiplication by 1/px (and rsqrt) instead of the
-    // canonical divisions; each floor/ceil is certain unless the fast value lies
-    // within 1e-9 px of an integer (fast vs canonical differ by ~1e-13 px), in
-    // which case the canonical O3 expression is evaluated exactly.
-    double ampfac = kSqrt2Pi * g.sdetS * rsqrt(det2);
-    double amp = rho * ampfac;
-    bool ok = g.ok != 0.0 && isfinite(mx) && isfinite(my) && isfinite(A) && isfinite(Cc) && isfinite(det2) &&
-              det2 > 0.0 && isfinite(amp);
+    const double mx = fma(W[0], mu0, fma(W[1], mu1, fma(W[2], mu2, tx)));
+    const double my = fma(W[3], mu0, fma(W[4], mu1, fma(W[5], mu2, ty)));
+    // fp32 fast path: Sigma_hat from the rotated frame as sums of positive terms (no
+    // cancellation): A = sum s_k p_k^2, C = sum s_k q_k^2, B = sum s_k p_k q_k, and by
+    // Cauchy-Binet det2 = sum_{k<l} s_k s_l (p_k q_l - p_l q_k)^2, p_k = W_0 . r_k, q_k = W_1 . r_k.
+    float p[3], q[3], s3[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float4 ck = g32.c[k];
+      p[k] = fmaf(Wf[0], ck.x, fmaf(Wf[1], ck.y, Wf[2] * ck.z));
+      q[k] = fmaf(Wf[3], ck.x, fmaf(Wf[4], ck.y, Wf[5] * ck.z));
+      s3[k] = ck.w;
+    }
+    const float Af = fmaf(s3[0], p[0] * p[0], fmaf(s3[1], p[1] * p[1], s3[2] * p[2] * p[2]));
+    const float Cf = fmaf(s3[0], q[0] * q[0], fmaf(s3[1], q[1] * q[1], s3[2] * q[2] * q[2]));
+    const float Bf = fmaf(s3[0], p[0] * q[0], fmaf(s3[1], p[1] * q[1], s3[2] * p[2] * q[2]));
+    const float x01 = fmaf(p[0], q[1], -p[1] * q[0]), x02 = fmaf(p[0], q[2], -p[2] * q[0]),
+                x12 = fmaf(p[1], q[2], -p[2] * q[1]);
+    const float d2f = fmaf(s3[0] * s3[1], x01 * x01, fmaf(s3[0] * s3[2], x02 * x02, s3[1] * s3[2] * x12 * x12));
+    const float rdet = rsqrt_approx(d2f * __frcp_rn(s3[0] * s3[1] * s3[2]));   // sqrt(|Sigma| / det2)
+    float ampf = (float)rho * 2.5066282746310002f * rdet;
     int ulo = 1, uhi = 0, vlo = 1, vhi = 0;
-    bool vis = false;
+    bool vis = false, exact = false;
+    float mxp = 0.f, myp = 0.f;
+    const bool okf = s3[0] >= 0.f && isfinite(Af) && isfinite(Cf) && d2f > 0.f && isfinite(d2f) &&
+                     isfinite(ampf) && isfinite(mx) && isfinite(my);
+    if (okf) {
+      const float rxp = kf * (Af * rsqrt_approx(Af)) * ipxf, ryp = kf * (Cf * rsqrt_approx(Cf)) * ipxf;
+      const double mxd = fma(mx, ipx, half), myd = fma(my, ipx, half);
+      const float cx = (float)mxd, cy = (float)myd;
+      const float fu0 = cx - rxp, fu1 = cx + rxp, fv0 = cy - ryp, fv1 = cy + ryp;
+      // fp32 error here is < 1e-4 px (positive sums, fp64 centre): a floor/ceil is certain
+      // unless the value lies within 1e-3 px of an integer -> canonical fp64 chain
+      const float e = 1e-3f;
+      exact = fabsf(fu0 - rintf(fu0)) < e || fabsf(fu1 - rintf(fu1)) < e || fabsf(fv0 - rintf(fv0)) < e ||
+              fabsf(fv1 - rintf(fv1)) < e;
+      if (tau > 0.0 && fabsf(fabsf(ampf) - (float)tau) <= 1e-4f * (float)tau) exact = true;
+      if (!exact) {
+        // clip as the canonical chain does: lo to [0, D], hi to [-1, D-1] (in float: no overflow)
+        const float Df = (float)c.D;
+        ulo = (int)fminf(fmaxf(ceilf(fu0), 0.f), Df);
+        uhi = (int)fmaxf(fminf(floorf(fu1), Df - 1.f), -1.f);
+        vlo = (int)fminf(fmaxf(ceilf(fv0), 0.f), Df);
+        vhi = (int)fmaxf(fminf(floorf(fv1), Df - 1.f), -1.f);
+        vis = fabsf(ampf) > (float)tau && ulo <= uhi && vlo <= vhi;
+        mxp = (float)(mxd - (double)ulo);
+        myp = (float)(myd - (double)vlo);
+      }
+    } else {
+      exact = s3[0] >= 0.f;   // degenerate-looking but valid frame: let fp64 decide
+    }
     SplatRec o;
     o.f0 = make_float4(0.f, 0.f, 0.f, 0.f);
     o.f1 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (ok) {
-      double rx = dm(kk, sqrt(A)), ry = dm(kk, sqrt(Cc));
-      const double fu0 = fma(mx - rx, ipx, half), fu1 = fma(mx + rx, ipx, half);
-      const double fv0 = fma(my - ry, ipx, half), fv1 = fma(my + ry, ipx, half);
-      double cu0 = ceil(fu0), cu1 = floor(fu1), cv0 = ceil(fv0), cv1 = floor(fv1);
-      const double eps = 1e-9;
-      if (fabs(fu0 - rint(fu0)) < eps || fabs(fu1 - rint(fu1)) < eps || fabs(fv0 - rint(fv0)) < eps ||
-          fabs(fv1 - rint(fv1)) < eps) {  // canonical O3 evaluation (rare)
-        cu0 = ceil(da(dv(dsb(mx, rx), px), half));
-        cu1 = floor(da(dv(da(mx, rx), px), half));
-        cv0 = ceil(da(dv(dsb(my, ry), px), half));
-        cv1 = floor(da(dv(da(my, ry), px), half));
+    float aa = 0.f, bb = 0.f, cc2 = 0.f;
+    if (exact) {   // canonical O3 chain in fp64: bit-identical to the oracle
+      const GaussPrep g = prep[j];
+      const double mxc = da(da(da(dm(W[0], mu0), dm(W[1], mu1)), dm(W[2], mu2)), tx);
+      const double myc = da(da(da(dm(W[3], mu0), dm(W[4], mu1)), dm(W[5], mu2)), ty);
+      const double S00 = g.sig[0], S01 = g.sig[1], S02 = g.sig[2], S11 = g.sig[3], S12 = g.sig[4], S22 = g.sig[5];
+      const double v00 = da(da(dm(S00, W[0]), dm(S01, W[1])), dm(S02, W[2]));
+      const double v01 = da(da(dm(S01, W[0]), dm(S11, W[1])), dm(S12, W[2]));
+      const double v02 = da(da(dm(S02, W[0]), dm(S12, W[1])), dm(S22, W[2]));
+      const double v10 = da(da(dm(S00, W[3]), dm(S01, W[4])), dm(S02, W[5]));
+      const double v11 = da(da(dm(S01, W[3]), dm(S11, W[4])), dm(S12, W[5]));
+      const double v12 = da(da(dm(S02, W[3]), dm(S12, W[4])), dm(S22, W[5]));
+      const double A = da(da(dm(W[0], v00), dm(W[1], v01)), dm(W[2], v02));
+      const double Bc = da(da(dm(W[0], v10), dm(W[1], v11)), dm(W[2], v12));
+      const double Cc = da(da(dm(W[3], v10), dm(W[4], v11)), dm(W[5], v12));
+      const double det2 = dsb(dm(A, Cc), dm(Bc, Bc));
+      const double ampc = dm(rho, dm(kSqrt2Pi, sqrt(dv(g.detS, det2))));
+      const bool ok = g.ok != 0.0 && isfinite(mxc) && isfinite(myc) && isfinite(A) && isfinite(Cc) &&
+                      isfinite(det2) && det2 > 0.0 && isfinite(ampc);
+      ulo = 1; uhi = 0; vlo = 1; vhi = 0;
+      vis = false;
+      if (ok) {
+        const double rx = dm(kk, sqrt(A)), ry = dm(kk, sqrt(Cc));
+        ulo = clip_d(ceil(da(dv(dsb(mxc, rx), px), half)), 0, c.D);
+        uhi = clip_d(floor(da(dv(da(mxc, rx), px), half)), -1, c.D - 1);
+        vlo = clip_d(ceil(da(dv(dsb(myc, ry), px), half)), 0, c.D);
+        vhi = clip_d(floor(da(dv(da(myc, ry), px), half)), -1, c.D - 1);
+        vis = fabs(ampc) > tau && ulo <= uhi && vlo <= vhi;
+        if (vis) {
+          mxp = (float)(fma(mx, ipx, half) - (double)ulo);
+          myp = (float)(fma(my, ipx, half) - (double)vlo);
+          const double px2 = px * px;
+          aa = (float)(Cc / det2 * px2);
+          bb = (float)(-Bc / det2 * px2);
+          cc2 = (float)(A / det2 * px2);
+          ampf = (float)ampc;
+        }
       }
-      ulo = clip_d(cu0, 0, c.D);
-      uhi = clip_d(cu1, -1, c.D - 1);
-      vlo = clip_d(cv0, 0, c.D);
-      vhi = clip_d(cv1, -1, c.D - 1);
-      bool above = fabs(amp) > tau;
-      if (tau > 0.0 && fabs(fabs(amp) - tau) <= 1e-12 * tau) {  // canonical amplitude near the threshold
-        const double ampc = dm(rho, dm(kSqrt2Pi, sqrt(dv(g.detS, det2))));
-        above = fabs(ampc) > tau;
-      }
-      vis = above && ulo <= uhi && vlo <= vhi;
+    } else if (vis) {
+      const float id2 = px2f / d2f;
+      aa = Cf * id2;
+      bb = -Bf * id2;
+      cc2 = Af * id2;
     }
     if (vis) {
-      const double px2 = px * px;
-      double mxp = fma(mx, ipx, half), myp = fma(my, ipx, half);
-      o.f0 = make_float4((float)(mxp - (double)ulo), (float)(myp - (double)vlo), (float)(Cc / det2 * px2),
-                         (float)(-Bc / det2 * px2));
-      o.f1 = make_float4((float)(A / det2 * px2), (float)amp, __int_as_float((ulo & 0xffff) | (uhi << 16)),
+      o.f0 = make_float4(mxp, myp, aa, bb);
+      o.f1 = make_float4(cc2, ampf, __int_as_float((ulo & 0xffff) | (uhi << 16)),
                          __int_as_float((vlo & 0xffff) | (vhi << 16)));
       pairs += (unsigned long long)(uhi - ulo + 1) * (unsigned long long)(vhi - vlo + 1);
       const int tu0 = (ulo >> c.tshift), tu1 = (uhi >> c.tshift), tv0 = (vlo >> c.tshift), tv1 = (vhi >> c.tshift);
