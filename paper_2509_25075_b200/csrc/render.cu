@@ -91,21 +91,35 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
     if ((int64_t)e > c.cap) e = (int)c.cap;
     if ((int64_t)s > c.cap) s = (int)c.cap;
     float *out = proj + (size_t)i * c.D * c.D;
+    if (s >= e) {   // empty tile: the projection is zero there
+      for (int p = lane; p < T * T; p += 32) {
+        const int u = u0 + p % T, v = v0 + p / T;
+        if (u < c.D && v < c.D) out[(size_t)v * c.D + u] = 0.f;
+      }
+      continue;
+    }
     float2 acc[T];
 #pragma unroll
     for (int k = 0; k < T; ++k) acc[k] = make_float2(0.f, 0.f);
     const SplatRec *reci = rec + (size_t)i * c.N;
-    for (int cs = s; cs < e; cs += kCH) {
-      const int n = min(kCH, e - cs);
-      int blen = 0;   // length of bin mp (lanes of pair pp hold bin pp's length)
-      for (int q0 = 0; q0 < n; q0 += 32) {
-        const int q = q0 + lane;
+    // software pipeline over 32-entry groups: ids two groups ahead, records one group ahead
+    const int nall = e - s;
+    int id1 = lane < nall ? ids[s + lane] : 0;
+    int id2 = 32 + lane < nall ? ids[s + 32 + lane] : 0;
+    SplatRec nxt;
+    if (lane < nall) nxt = reci[id1];
+    int blen = 0;   // length of bin mp in the current chunk (lanes of pair pp hold bin pp's length)
+    for (int g0 = 0; g0 < nall; g0 += 32) {
+      const int q = g0 + lane;
+      const SplatRec rr = nxt;
+      if (q + 32 < nall) nxt = reci[id2];
+      if (q + 64 < nall) id2 = ids[s + q + 64];
+      {
         int pr0 = NP, pr1 = -1, cu0 = 0, cu1 = 0, cv0 = 0, cv1 = 0;
         bool slow = false, neg = false;
         float El = 0.f, V = 0.f, Rl = 0.f, W = 0.f, Kb = 0.f, S = 0.f, na = 0.f, nb2 = 0.f, nc = 0.f, Fx = 0.f,
               Gx = 0.f, D0 = 0.f, my = 0.f, la = 0.f;
-        if (q < n) {
-          const SplatRec rr = reci[ids[cs + q]];
+        if (q < nall) {
           const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
           const int ulo = (ub & 0xffff) - u0, uhi = (ub >> 16) - u0, vlo = (vb & 0xffff) - v0, vhi = (vb >> 16) - v0;
           cu0 = max(ulo, 0); cu1 = min(uhi, T - 1); cv0 = max(vlo, 0); cv1 = min(vhi, T - 1);
@@ -161,6 +175,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
           if (mp == pp) blen += __popc(bal);
         }
       }
+      if ((g0 + 32) % kCH != 0 && g0 + 32 < nall) continue;   // the chunk's bins are not full yet
       __syncwarp();
       // render: lanes of pair mp take segments cp, cp + NCP, ... of bin mp
 #pragma unroll 1
@@ -194,6 +209,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
           }
         }
       }
+      blen = 0;
       __syncwarp();
     }
     // sum the NCP copies of each pair-row (fixed butterfly), lane cp writes columns cp, cp + NCP, ...
@@ -281,10 +297,11 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, const SplatR
       R2.y = vB ? Rl : 0.f;
       if (vB) { El *= V; V *= W; Rl *= Kb; }
       float2 kk = make_float2(0.f, 0.f);
-#pragma unroll 2
-      for (int k = 0; k < wd; ++k) {
-        const float2 g2 = make_float2(__ldg(ga + k), vB ? __ldg(gb + k) : 0.f);
-        const float2 h = __fmul2_rn(g2, E2);
+      // column pairs at even absolute columns are read with one 64-bit load per row (half the
+      // L1 requests); an odd first column and an odd last column are peeled
+      int k = 0;
+      auto step = [&](float gA, float gBv) {
+        const float2 h = __fmul2_rn(make_float2(gA, gBv), E2);
         const float2 hk = __fmul2_rn(h, kk);
         T0 = __fadd2_rn(T0, h);
         T1 = __fadd2_rn(T1, hk);
@@ -292,7 +309,19 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, const SplatR
         E2 = __fmul2_rn(E2, R2);
         R2 = __fmul2_rn(R2, S2);
         kk = __fadd2_rn(kk, one);
+      };
+      if (ulo & 1) {
+        step(__ldg(ga), vB ? __ldg(gb) : 0.f);
+        k = 1;
       }
+#pragma unroll 1
+      for (; k + 1 < wd; k += 2) {
+        const float2 a2 = __ldg(reinterpret_cast<const float2 *>(ga + k));
+        const float2 b2 = vB ? __ldg(reinterpret_cast<const float2 *>(gb + k)) : make_float2(0.f, 0.f);
+        step(a2.x, b2.x);
+        step(a2.y, b2.y);
+      }
+      if (k < wd) step(__ldg(ga + k), vB ? __ldg(gb + k) : 0.f);
     } else {   // direct evaluation, exp per pixel
       const float fA = fmaf(dyA, fmaf(nc, dyA, Gx), Fx), fB = fmaf(dyB, fmaf(nc, dyB, Gx), Fx);
       const float gA = fmaf(nb2, dyA, D0), gB = fmaf(nb2, dyB, D0);
