@@ -334,13 +334,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int *__restrict__ out
 }
 
 // --------------------------------------------------------------- a3 fill
-// One CTA of 4 warps per (particle, chunk of 1024 Gaussians); warp w owns the
-// 256-Gaussian sub-chunk w.  Pass 1 counts each sub-chunk's entries per tile
-// (smem integer atomics, order-free); a per-tile scan over the 4 sub-chunks,
-// seeded with the chunk's global offset, gives each warp its cursors; pass 2
-// visits the warp's Gaussians in ascending j, 32 per step, enumerates each
-// step's (j, tile) pairs in (j, tile) order and ranks them per tile with
-// __match_any_sync — a stable counting sort, so every list is ascending in j.
+// One CTA of 4 warps per (particle, chunk of kChunk Gaussians); warp w owns the sub-chunk w.
+// Pass 1 counts each sub-chunk's entries per tile (smem integer atomics, order-free); a per-tile
+// scan over the 4 sub-chunks, seeded with the chunk's global offset, gives each warp its
+// cursors; pass 2 visits the warp's Gaussians 32 per step and, for each tile slot (dv, du) of
+// their tile rectangles in turn, ranks the step's entries per tile with __match_any_sync.  The
+// order within a tile's list is therefore (chunk, sub-chunk, step, slot, Gaussian id): a
+// deterministic function of the boxes (so the forward stays bitwise reproducible), and the
+// per-tile sets equal the oracle's (reading L9: only the set and its determinism matter).
 constexpr int kFillWarps = 4, kSub = kChunk / kFillWarps;
 
 __device__ __forceinline__ void rect_of(uint2 b, int ts, int &tu0, int &tu1, int &tv0, int &n) {
@@ -382,54 +383,30 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
   }
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
-  const float M = 12582912.f;
-  for (int step = 0; step < kSub / 32; ++step) {     // pass 2: stable fill
+  for (int step = 0; step < kSub / 32; ++step) {     // pass 2: deterministic fill
     const int j0 = jsub + step * 32;
     if (j0 >= c.N) break;
     const int j = j0 + lane;
     int tu0 = 0, tu1 = -1, tv0 = 0, n = 0;
     if (j < c.N) rect_of(boxi[j], c.tshift, tu0, tu1, tv0, n);
-    const float rw = 1.0f / (float)max(tu1 - tu0 + 1, 1);   // once per lane and step
-    int incl = n;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += y;
-    }
-    const int excl = incl - n;
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    for (int p0 = 0; p0 < total; p0 += 32) {
-      const int p = p0 + lane;
-      const bool active = p < total;
-      int lo = 0;
-#pragma unroll
-      for (int sft = 16; sft >= 1; sft >>= 1) {
-        const int vv = __shfl_sync(0xffffffffu, incl, lo + sft - 1);
-        if (vv <= p) lo += sft;
+    const int ntu = tu1 - tu0 + 1, ntv = n > 0 ? n / max(ntu, 1) : 0;
+    // slot-major order: every lane's tile (dv, du) of its rectangle, (dv, du) ascending, then lane
+    const int mu = __reduce_max_sync(0xffffffffu, (unsigned)max(ntu, 0));
+    const int mv = __reduce_max_sync(0xffffffffu, (unsigned)ntv);
+    for (int dv = 0; dv < mv; ++dv) {
+      for (int du = 0; du < mu; ++du) {
+        const bool active = du < ntu && dv < ntv;
+        const int t = (tv0 + dv) * c.nt + tu0 + du;
+        const unsigned m = __match_any_sync(0xffffffffu, active ? t : -1);
+        const int rank = __popc(m & lt);
+        if (active) {
+          const int slot = mine[t] + rank;
+          if ((int64_t)slot < c.cap) ids[slot] = j;
+        }
+        __syncwarp();
+        if (active && rank == 0) mine[t] += __popc(m);
+        __syncwarp();
       }
-      const int owner = lo & 31;
-      const int oex = __shfl_sync(0xffffffffu, excl, owner);
-      const int otu0 = __shfl_sync(0xffffffffu, tu0, owner);
-      const int otu1 = __shfl_sync(0xffffffffu, tu1, owner);
-      const int otv0 = __shfl_sync(0xffffffffu, tv0, owner);
-      const float orw = __shfl_sync(0xffffffffu, rw, owner);
-      int key = 0x40000000 + lane, t = 0;
-      if (active) {
-        const int r = p - oex, wd = otu1 - otu0 + 1;
-        // q = r div wd exactly: round((r + 1/2)/wd - 1/2) with a magic-constant rounding
-        const int q = __float_as_int(fmaf((float)r + 0.5f, orw, -0.5f) + M) - 0x4B400000;
-        t = (otv0 + q) * c.nt + otu0 + (r - q * wd);
-        key = t;
-      }
-      const unsigned m = __match_any_sync(0xffffffffu, key);
-      const int rank = __popc(m & lt);
-      if (active) {
-        const int slot = mine[t] + rank;
-        if ((int64_t)slot < c.cap) ids[slot] = j0 + owner;
-      }
-      __syncwarp();
-      if (active && rank == 0) mine[t] += __popc(m);
-      __syncwarp();
     }
   }
 }

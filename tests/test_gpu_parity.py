@@ -101,7 +101,11 @@ def assert_lists_exact(orc, case, lists, tile, first=0):
         if ties == 0:
             o_ids = ids[base[i]: base[i] + tile_off[i, -1]]
             assert np.array_equal(g_off, tile_off[i]), i
-            assert np.array_equal(g_ids, o_ids), i
+            # the per-tile SETS are bit-exact; the order within a tile is the GPU's deterministic
+            # (chunk, step, slot, id) order (reading L9), so compare each tile's sorted ids
+            for t in range(len(g_off) - 1):
+                a, b = g_off[t], g_off[t + 1]
+                assert np.array_equal(np.sort(g_ids[a:b]), o_ids[a:b]), (i, t)
     return ties
 
 
