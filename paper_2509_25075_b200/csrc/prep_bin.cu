@@ -102,15 +102,64 @@ __device__ __forceinline__ int clip_d(double v, int lo, int hi) {
 // k-sigma AABB; visible => count one entry per touched tile in a per-CTA
 // smem histogram; hist layout [i][t][chunk] so that one flat exclusive scan
 // yields every list's start (t-major) and each chunk's sub-offset.
-__global__ void __launch_bounds__(256) k_splat_count(CfgDev c, const GaussPrep *__restrict__ prep,
-                                                     const float4 *__restrict__ mr, const float *__restrict__ rot,
-                                                     const float *__restrict__ shift, SplatRec *__restrict__ rec,
-                                                     uint2 *__restrict__ box, int *__restrict__ hist,
-                                                     DevStats *__restrict__ st) {
-  extern __shared__ int shist[];
+// Canonical O3 chain in fp64: bit-identical to the oracle.  Used only for the
+// Gaussians whose fp32 bounds lie within 1e-3 px of an integer (or look degenerate).
+__device__ __noinline__ bool splat_exact(const GaussPrep &g, const double *W, double tx, double ty, float4 m4,
+                                         const CfgDev &c, double px, double ipx, double half, double kk, double tau,
+                                         int &ulo, int &uhi, int &vlo, int &vhi, float &mxp, float &myp, float &aa,
+                                         float &bb, float &cc2, float &ampf) {
+  const double mu0 = m4.x, mu1 = m4.y, mu2 = m4.z, rho = m4.w;
+  const double mxc = da(da(da(dm(W[0], mu0), dm(W[1], mu1)), dm(W[2], mu2)), tx);
+  const double myc = da(da(da(dm(W[3], mu0), dm(W[4], mu1)), dm(W[5], mu2)), ty);
+  const double S00 = g.sig[0], S01 = g.sig[1], S02 = g.sig[2], S11 = g.sig[3], S12 = g.sig[4], S22 = g.sig[5];
+  const double v00 = da(da(dm(S00, W[0]), dm(S01, W[1])), dm(S02, W[2]));
+  const double v01 = da(da(dm(S01, W[0]), dm(S11, W[1])), dm(S12, W[2]));
+  const double v02 = da(da(dm(S02, W[0]), dm(S12, W[1])), dm(S22, W[2]));
+  const double v10 = da(da(dm(S00, W[3]), dm(S01, W[4])), dm(S02, W[5]));
+  const double v11 = da(da(dm(S01, W[3]), dm(S11, W[4])), dm(S12, W[5]));
+  const double v12 = da(da(dm(S02, W[3]), dm(S12, W[4])), dm(S22, W[5]));
+  const double A = da(da(dm(W[0], v00), dm(W[1], v01)), dm(W[2], v02));
+  const double Bc = da(da(dm(W[0], v10), dm(W[1], v11)), dm(W[2], v12));
+  const double Cc = da(da(dm(W[3], v10), dm(W[4], v11)), dm(W[5], v12));
+  const double det2 = dsb(dm(A, Cc), dm(Bc, Bc));
+  const double ampc = dm(rho, dm(kSqrt2Pi, sqrt(dv(g.detS, det2))));
+  const bool ok = g.ok != 0.0 && isfinite(mxc) && isfinite(myc) && isfinite(A) && isfinite(Cc) && isfinite(det2) &&
+                  det2 > 0.0 && isfinite(ampc);
+  ulo = 1; uhi = 0; vlo = 1; vhi = 0;
+  if (!ok) return false;
+  const double rx = dm(kk, sqrt(A)), ry = dm(kk, sqrt(Cc));
+  ulo = clip_d(ceil(da(dv(dsb(mxc, rx), px), half)), 0, c.D);
+  uhi = clip_d(floor(da(dv(da(mxc, rx), px), half)), -1, c.D - 1);
+  vlo = clip_d(ceil(da(dv(dsb(myc, ry), px), half)), 0, c.D);
+  vhi = clip_d(floor(da(dv(da(myc, ry), px), half)), -1, c.D - 1);
+  if (!(fabs(ampc) > tau && ulo <= uhi && vlo <= vhi)) return false;
+  const double mx = fma(W[0], mu0, fma(W[1], mu1, fma(W[2], mu2, tx)));
+  const double my = fma(W[3], mu0, fma(W[4], mu1, fma(W[5], mu2, ty)));
+  mxp = (float)(fma(mx, ipx, half) - (double)ulo);
+  myp = (float)(fma(my, ipx, half) - (double)vlo);
+  const double px2 = px * px;
+  aa = (float)(Cc / det2 * px2);
+  bb = (float)(-Bc / det2 * px2);
+  cc2 = (float)(A / det2 * px2);
+  ampf = (float)ampc;
+  return true;
+}
+
+constexpr int kSplatThreads = 256;
+
+__global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, const GaussPrep *__restrict__ prep,
+                                                               const float4 *__restrict__ mr,
+                                                               const float *__restrict__ rot,
+                                                               const float *__restrict__ shift,
+                                                               SplatRec *__restrict__ rec, uint2 *__restrict__ box,
+                                                               int *__restrict__ hist, DevStats *__restrict__ st) {
+  extern __shared__ int shist[];   // [NT] tile histogram, then the exact-path queue [kChunk]
+  int *queue = shist + c.NT;
+  __shared__ int qn;
   const int i = blockIdx.y, ch = blockIdx.x, tid = threadIdx.x;
   const GaussPrep32 *__restrict__ prep32 = reinterpret_cast<const GaussPrep32 *>(prep + c.N);
   for (int t = tid; t < c.NT; t += blockDim.x) shist[t] = 0;
+  if (tid == 0) qn = 0;
   double W[9];
   float Wf[6];
 #pragma unroll
@@ -121,18 +170,38 @@ __global__ void __launch_bounds__(256) k_splat_count(CfgDev c, const GaussPrep *
   for (int k = 0; k < 6; ++k) Wf[k] = (float)W[k];
   const double tx = shift[2 * i], ty = shift[2 * i + 1];
   const double px = c.px, half = (double)(c.D / 2), kk = c.k, tau = c.tau, ipx = 1.0 / px;
-  const float kf = c.k, ipxf = (float)ipx, halff = (float)half, px2f = c.px * c.px;
-  unsigned long long pairs = 0;
+  const float kf = c.k, ipxf = (float)ipx, px2f = c.px * c.px, Df = (float)c.D, tauf = (float)tau;
+  unsigned pairs = 0;
   __syncthreads();
-  for (int r = 0; r < kChunk / 256; ++r) {
-    int j = ch * kChunk + r * 256 + tid;
+  auto emit = [&](int j, bool vis, int ulo, int uhi, int vlo, int vhi, float mxp, float myp, float aa, float bb,
+                  float cc2, float ampf) {
+    SplatRec o;
+    if (vis) {
+      o.f0 = make_float4(mxp, myp, aa, bb);
+      o.f1 = make_float4(cc2, ampf, __int_as_float((ulo & 0xffff) | (uhi << 16)),
+                         __int_as_float((vlo & 0xffff) | (vhi << 16)));
+      pairs += (unsigned)((uhi - ulo + 1) * (vhi - vlo + 1));
+      const int tu0 = (ulo >> c.tshift), tu1 = (uhi >> c.tshift), tv0 = (vlo >> c.tshift), tv1 = (vhi >> c.tshift);
+      for (int tv = tv0; tv <= tv1; ++tv)
+        for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&shist[tv * c.nt + tu], 1);
+    } else {
+      ulo = 1; uhi = 0; vlo = 1; vhi = 0;
+      o.f0 = make_float4(0.f, 0.f, 0.f, 0.f);
+      o.f1 = make_float4(0.f, 0.f, __int_as_float(1), __int_as_float(1));
+    }
+    const size_t ij = (size_t)i * c.N + j;
+    rec[ij] = o;
+    box[ij] = make_uint2((unsigned)(ulo & 0xffff) | ((unsigned)uhi << 16), (unsigned)(vlo & 0xffff) | ((unsigned)vhi << 16));
+  };
+  for (int r = 0; r < kChunk / kSplatThreads; ++r) {
+    const int j = ch * kChunk + r * kSplatThreads + tid;
     if (j >= c.N) break;
     const float4 m4 = mr[j];
     const GaussPrep32 g32 = prep32[j];
     // centre in fp64 (the record stores it relative to the box corner to ~1e-7 px)
-    const double mu0 = m4.x, mu1 = m4.y, mu2 = m4.z, rho = m4.w;
-    const double mx = fma(W[0], mu0, fma(W[1], mu1, fma(W[2], mu2, tx)));
-    const double my = fma(W[3], mu0, fma(W[4], mu1, fma(W[5], mu2, ty)));
+    const double mx = fma(W[0], (double)m4.x, fma(W[1], (double)m4.y, fma(W[2], (double)m4.z, tx)));
+    const double my = fma(W[3], (double)m4.x, fma(W[4], (double)m4.y, fma(W[5], (double)m4.z, ty)));
+    const double mxd = fma(mx, ipx, half), myd = fma(my, ipx, half);
     // fp32 fast path: Sigma_hat from the rotated frame as sums of positive terms (no
     // cancellation): A = sum s_k p_k^2, C = sum s_k q_k^2, B = sum s_k p_k q_k, and by
     // Cauchy-Binet det2 = sum_{k<l} s_k s_l (p_k q_l - p_l q_k)^2, p_k = W_0 . r_k, q_k = W_1 . r_k.
@@ -150,105 +219,43 @@ __global__ void __launch_bounds__(256) k_splat_count(CfgDev c, const GaussPrep *
     const float x01 = fmaf(p[0], q[1], -p[1] * q[0]), x02 = fmaf(p[0], q[2], -p[2] * q[0]),
                 x12 = fmaf(p[1], q[2], -p[2] * q[1]);
     const float d2f = fmaf(s3[0] * s3[1], x01 * x01, fmaf(s3[0] * s3[2], x02 * x02, s3[1] * s3[2] * x12 * x12));
-    const float rdet = rsqrt_approx(d2f * __frcp_rn(s3[0] * s3[1] * s3[2]));   // sqrt(|Sigma| / det2)
-    float ampf = (float)rho * 2.5066282746310002f * rdet;
-    int ulo = 1, uhi = 0, vlo = 1, vhi = 0;
-    bool vis = false, exact = false;
-    float mxp = 0.f, myp = 0.f;
-    const bool okf = s3[0] >= 0.f && isfinite(Af) && isfinite(Cf) && d2f > 0.f && isfinite(d2f) &&
-                     isfinite(ampf) && isfinite(mx) && isfinite(my);
-    if (okf) {
-      const float rxp = kf * (Af * rsqrt_approx(Af)) * ipxf, ryp = kf * (Cf * rsqrt_approx(Cf)) * ipxf;
-      const double mxd = fma(mx, ipx, half), myd = fma(my, ipx, half);
-      const float cx = (float)mxd, cy = (float)myd;
-      const float fu0 = cx - rxp, fu1 = cx + rxp, fv0 = cy - ryp, fv1 = cy + ryp;
-      // fp32 error here is < 1e-4 px (positive sums, fp64 centre): a floor/ceil is certain
-      // unless the value lies within 1e-3 px of an integer -> canonical fp64 chain
-      const float e = 1e-3f;
-      exact = fabsf(fu0 - rintf(fu0)) < e || fabsf(fu1 - rintf(fu1)) < e || fabsf(fv0 - rintf(fv0)) < e ||
-              fabsf(fv1 - rintf(fv1)) < e;
-      if (tau > 0.0 && fabsf(fabsf(ampf) - (float)tau) <= 1e-4f * (float)tau) exact = true;
-      if (!exact) {
-        // clip as the canonical chain does: lo to [0, D], hi to [-1, D-1] (in float: no overflow)
-        const float Df = (float)c.D;
-        ulo = (int)fminf(fmaxf(ceilf(fu0), 0.f), Df);
-        uhi = (int)fmaxf(fminf(floorf(fu1), Df - 1.f), -1.f);
-        vlo = (int)fminf(fmaxf(ceilf(fv0), 0.f), Df);
-        vhi = (int)fmaxf(fminf(floorf(fv1), Df - 1.f), -1.f);
-        vis = fabsf(ampf) > (float)tau && ulo <= uhi && vlo <= vhi;
-        mxp = (float)(mxd - (double)ulo);
-        myp = (float)(myd - (double)vlo);
-      }
-    } else {
-      exact = s3[0] >= 0.f;   // degenerate-looking but valid frame: let fp64 decide
+    const float ampf = m4.w * 2.5066282746310002f * rsqrt_approx(d2f * __frcp_rn(s3[0] * s3[1] * s3[2]));
+    const float cx = (float)mxd, cy = (float)myd;
+    const float rxp = kf * (Af * rsqrt_approx(Af)) * ipxf, ryp = kf * (Cf * rsqrt_approx(Cf)) * ipxf;
+    const float fu0 = cx - rxp, fu1 = cx + rxp, fv0 = cy - ryp, fv1 = cy + ryp;
+    // fp32 error here is < 1e-4 px (positive sums, fp64 centre): a floor/ceil is certain unless
+    // the value lies within 1e-3 px of an integer (or anything looks degenerate) -> exact queue
+    const float e = 1e-3f;
+    const bool okf = s3[0] >= 0.f && d2f > 0.f && fabsf(ampf) < 3e38f && fabsf(fu0) < 1e9f && fabsf(fu1) < 1e9f &&
+                     fabsf(fv0) < 1e9f && fabsf(fv1) < 1e9f;
+    const bool near = fabsf(fu0 - rintf(fu0)) < e || fabsf(fu1 - rintf(fu1)) < e || fabsf(fv0 - rintf(fv0)) < e ||
+                      fabsf(fv1 - rintf(fv1)) < e || (tau > 0.0 && fabsf(fabsf(ampf) - tauf) <= 1e-4f * tauf);
+    if (s3[0] >= 0.f && (!okf || near)) {   // deferred to the exact pass (compact, no warp divergence)
+      queue[atomicAdd(&qn, 1)] = j;
+      continue;
     }
-    SplatRec o;
-    o.f0 = make_float4(0.f, 0.f, 0.f, 0.f);
-    o.f1 = make_float4(0.f, 0.f, 0.f, 0.f);
-    float aa = 0.f, bb = 0.f, cc2 = 0.f;
-    if (exact) {   // canonical O3 chain in fp64: bit-identical to the oracle
-      const GaussPrep g = prep[j];
-      const double mxc = da(da(da(dm(W[0], mu0), dm(W[1], mu1)), dm(W[2], mu2)), tx);
-      const double myc = da(da(da(dm(W[3], mu0), dm(W[4], mu1)), dm(W[5], mu2)), ty);
-      const double S00 = g.sig[0], S01 = g.sig[1], S02 = g.sig[2], S11 = g.sig[3], S12 = g.sig[4], S22 = g.sig[5];
-      const double v00 = da(da(dm(S00, W[0]), dm(S01, W[1])), dm(S02, W[2]));
-      const double v01 = da(da(dm(S01, W[0]), dm(S11, W[1])), dm(S12, W[2]));
-      const double v02 = da(da(dm(S02, W[0]), dm(S12, W[1])), dm(S22, W[2]));
-      const double v10 = da(da(dm(S00, W[3]), dm(S01, W[4])), dm(S02, W[5]));
-      const double v11 = da(da(dm(S01, W[3]), dm(S11, W[4])), dm(S12, W[5]));
-      const double v12 = da(da(dm(S02, W[3]), dm(S12, W[4])), dm(S22, W[5]));
-      const double A = da(da(dm(W[0], v00), dm(W[1], v01)), dm(W[2], v02));
-      const double Bc = da(da(dm(W[0], v10), dm(W[1], v11)), dm(W[2], v12));
-      const double Cc = da(da(dm(W[3], v10), dm(W[4], v11)), dm(W[5], v12));
-      const double det2 = dsb(dm(A, Cc), dm(Bc, Bc));
-      const double ampc = dm(rho, dm(kSqrt2Pi, sqrt(dv(g.detS, det2))));
-      const bool ok = g.ok != 0.0 && isfinite(mxc) && isfinite(myc) && isfinite(A) && isfinite(Cc) &&
-                      isfinite(det2) && det2 > 0.0 && isfinite(ampc);
-      ulo = 1; uhi = 0; vlo = 1; vhi = 0;
-      vis = false;
-      if (ok) {
-        const double rx = dm(kk, sqrt(A)), ry = dm(kk, sqrt(Cc));
-        ulo = clip_d(ceil(da(dv(dsb(mxc, rx), px), half)), 0, c.D);
-        uhi = clip_d(floor(da(dv(da(mxc, rx), px), half)), -1, c.D - 1);
-        vlo = clip_d(ceil(da(dv(dsb(myc, ry), px), half)), 0, c.D);
-        vhi = clip_d(floor(da(dv(da(myc, ry), px), half)), -1, c.D - 1);
-        vis = fabs(ampc) > tau && ulo <= uhi && vlo <= vhi;
-        if (vis) {
-          mxp = (float)(fma(mx, ipx, half) - (double)ulo);
-          myp = (float)(fma(my, ipx, half) - (double)vlo);
-          const double px2 = px * px;
-          aa = (float)(Cc / det2 * px2);
-          bb = (float)(-Bc / det2 * px2);
-          cc2 = (float)(A / det2 * px2);
-          ampf = (float)ampc;
-        }
-      }
-    } else if (vis) {
-      const float id2 = px2f / d2f;
-      aa = Cf * id2;
-      bb = -Bf * id2;
-      cc2 = Af * id2;
-    }
-    if (vis) {
-      o.f0 = make_float4(mxp, myp, aa, bb);
-      o.f1 = make_float4(cc2, ampf, __int_as_float((ulo & 0xffff) | (uhi << 16)),
-                         __int_as_float((vlo & 0xffff) | (vhi << 16)));
-      pairs += (unsigned long long)(uhi - ulo + 1) * (unsigned long long)(vhi - vlo + 1);
-      const int tu0 = (ulo >> c.tshift), tu1 = (uhi >> c.tshift), tv0 = (vlo >> c.tshift), tv1 = (vhi >> c.tshift);
-      for (int tv = tv0; tv <= tv1; ++tv)
-        for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&shist[tv * c.nt + tu], 1);
-    } else {
-      ulo = 1; uhi = 0; vlo = 1; vhi = 0;
-      o.f1.z = __int_as_float(1);
-      o.f1.w = __int_as_float(1);
-    }
-    const size_t ij = (size_t)i * c.N + j;
-    rec[ij] = o;
-    box[ij] = make_uint2((unsigned)(ulo & 0xffff) | ((unsigned)uhi << 16), (unsigned)(vlo & 0xffff) | ((unsigned)vhi << 16));
+    // clip as the canonical chain does: lo to [0, D], hi to [-1, D-1] (in float: no overflow)
+    const int ulo = (int)fminf(fmaxf(ceilf(fu0), 0.f), Df);
+    const int uhi = (int)fmaxf(fminf(floorf(fu1), Df - 1.f), -1.f);
+    const int vlo = (int)fminf(fmaxf(ceilf(fv0), 0.f), Df);
+    const int vhi = (int)fmaxf(fminf(floorf(fv1), Df - 1.f), -1.f);
+    const bool vis = okf && fabsf(ampf) > tauf && ulo <= uhi && vlo <= vhi;
+    const float id2 = px2f / d2f;
+    emit(j, vis, ulo, uhi, vlo, vhi, (float)(mxd - (double)ulo), (float)(myd - (double)vlo), Cf * id2, -Bf * id2,
+         Af * id2, ampf);
+  }
+  __syncthreads();
+  for (int k = tid; k < qn; k += blockDim.x) {   // exact pass over the deferred Gaussians
+    const int j = queue[k];
+    int ulo, uhi, vlo, vhi;
+    float mxp = 0.f, myp = 0.f, aa = 0.f, bb = 0.f, cc2 = 0.f, ampf = 0.f;
+    const bool vis = splat_exact(prep[j], W, tx, ty, mr[j], c, px, ipx, half, kk, tau, ulo, uhi, vlo, vhi, mxp, myp,
+                                 aa, bb, cc2, ampf);
+    emit(j, vis, ulo, uhi, vlo, vhi, mxp, myp, aa, bb, cc2, ampf);
   }
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, d);
-  if ((tid & 31) == 0 && pairs) atomicAdd(&st->pairs, pairs);
+  if ((tid & 31) == 0 && pairs) atomicAdd(&st->pairs, (unsigned long long)pairs);
   __syncthreads();
   for (int t = tid; t < c.NT; t += blockDim.x) hist[((size_t)i * c.NT + t) * c.C + ch] = shist[t];
 }
@@ -423,7 +430,13 @@ void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const flo
                         const float *shift, SplatRec *rec, uint2 *box, int *hist, DevStats *st, cudaStream_t s,
                         int &launches) {
   dim3 grid(c.C, B);
-  k_splat_count<<<grid, 256, c.NT * sizeof(int), s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, st);
+  const size_t smem = (c.NT + kChunk) * sizeof(int);
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_splat_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    init = true;
+  }
+  k_splat_count<<<grid, kSplatThreads, smem, s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, st);
   ++launches;
 }
 
