@@ -16,29 +16,30 @@ namespace {
 constexpr int kCtfThreads = 256;
 constexpr double kPi = 3.14159265358979323846;
 
-// Per-particle constants: chi(f) = K1s s^2 + K1d ast(f) - K2 s^4 + phi, with
-// s^2 = fx^2 + fy^2, ast = (fx^2 - fy^2) cos 2θ + 2 fx fy sin 2θ,
-// K1s = π λ (du + dv)/2, K1d = π λ (du - dv)/2, K2 = π Cs λ^3 / 2 — the CTFFIND
-// form of reading L10 with Δf s^2 expanded (no division by s^2).
+// Per-particle constants.  With integer frequency indices (kx, ky) and idpx = 1/(D px):
+//   s^2 = n2 idpx^2, n2 = kx^2 + ky^2 (exact integer), ast s^2-terms = ((kx^2 - ky^2) cos 2θ +
+//   2 kx ky sin 2θ) idpx^2, so the CTFFIND phase of reading L10,
+//   chi = K1s s^2 + K1d ast - K2 s^4 + phi,
+// becomes chi = a n2 + b d2 + c m2 - e n2^2 + phi with d2 = kx^2 - ky^2, m2 = 2 kx ky (exact
+// integers) and per-particle fp64 coefficients: 4 DFMA per bin.  The phase (up to ~420 rad at
+// D = 256) is reduced mod 2 pi in fp64, then fp32 sincos on [-pi, pi].
 struct CtfP {
-  double K1s, K1d, K2, c2, s2a, phi;
-  float alpha_s, alpha_c, bq;   // sqrt(1 - α^2), α, B/4
+  double a, b, c, e, phi;
+  float alpha_s, alpha_c, bq;   // sqrt(1 - α^2), α, B idpx^2 / 4 (envelope exp(-bq n2))
 };
 
-__device__ __forceinline__ float ctf_raw(const CtfP &p, double fx, double fy) {
-  const double fx2 = fx * fx, fy2 = fy * fy, s2 = fx2 + fy2;
-  const double ast = fma(fx2 - fy2, p.c2, 2.0 * fx * fy * p.s2a);
-  double chi = fma(s2, fma(-p.K2, s2, p.K1s), fma(p.K1d, ast, p.phi));
+__device__ __forceinline__ float ctf_raw(const CtfP &p, double n2, double d2, double m2) {
+  double chi = fma(n2, fma(-p.e, n2, p.a), fma(p.b, d2, fma(p.c, m2, p.phi)));
   const double n = rint(chi * 0.15915494309189535);   // 1 / (2 pi)
   chi = fma(-n, 6.283185307179586, chi);                // reduced to [-pi, pi]
   float sn, cs;
   __sincosf((float)chi, &sn, &cs);                       // |abs err| < 4e-7 on [-pi, pi]
-  const float env = p.bq > 0.f ? __expf(-p.bq * (float)s2) : 1.f;
+  const float env = p.bq > 0.f ? __expf(-p.bq * (float)n2) : 1.f;
   return -env * (p.alpha_s * sn + p.alpha_c * cs);
 }
 
 // Per-particle CTF constants (fp64: wavelength, defocus, Cs, astigmatism), once per particle.
-__global__ void k_ctf_params(int B, const float *__restrict__ ctf, CtfP *__restrict__ out) {
+__global__ void k_ctf_params(int B, double idpx, const float *__restrict__ ctf, CtfP *__restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B) return;
   const float *q = ctf + 8 * i;
@@ -46,19 +47,26 @@ __global__ void k_ctf_params(int B, const float *__restrict__ ctf, CtfP *__restr
   const double h = 6.62607015e-34, m0 = 9.1093837015e-31, e = 1.602176634e-19, cl = 299792458.0;
   const double lam = h / sqrt(2.0 * m0 * e * V * (1.0 + e * V / (2.0 * m0 * cl * cl))) * 1e10;
   const double du = q[0], dv = q[1];
+  const double K1s = kPi * lam * 0.5 * (du + dv), K1d = kPi * lam * 0.5 * (du - dv);
+  const double K2 = 0.5 * kPi * ((double)q[4] * 1e7) * lam * lam * lam;
+  const double i2 = idpx * idpx;
   CtfP P;
-  P.K1s = kPi * lam * 0.5 * (du + dv);
-  P.K1d = kPi * lam * 0.5 * (du - dv);
-  P.K2 = 0.5 * kPi * ((double)q[4] * 1e7) * lam * lam * lam;
-  P.c2 = cos(2.0 * (double)q[2]);
-  P.s2a = sin(2.0 * (double)q[2]);
+  P.a = K1s * i2;
+  P.b = K1d * cos(2.0 * (double)q[2]) * i2;
+  P.c = K1d * sin(2.0 * (double)q[2]) * i2;
+  P.e = K2 * i2 * i2;
   P.phi = q[6];
   const double al = q[5];
   P.alpha_s = (float)sqrt(1.0 - al * al);
   P.alpha_c = (float)al;
-  P.bq = 0.25f * q[7];
+  P.bq = (float)(0.25 * (double)q[7] * i2);
   out[i] = P;
 }
+
+// One block per (particle, kCtfRows rows of ky); the block's Hx x kCtfRows bins are spread over
+// its threads (row = floor((idx + 1/2) / Hx) in fp32, exact at these sizes).  The loss is
+// summed in fp32 over a thread's few bins, then in fp64 (fixed tree) across the block.
+constexpr int kCtfRows = 8;
 
 __global__ void __launch_bounds__(kCtfThreads) k_ctf_loss(CfgDev c, const CtfP *__restrict__ ctfp,
                                                           float2 *__restrict__ spec_hat,
@@ -67,37 +75,37 @@ __global__ void __launch_bounds__(kCtfThreads) k_ctf_loss(CfgDev c, const CtfP *
   __shared__ double red[kCtfThreads / 32];
   const int i = blockIdx.y, tid = threadIdx.x;
   const CtfP P = ctfp[i];
-  const int D = c.D, Hx = D / 2 + 1;
-  const int H = D * Hx;
-  const int idx = blockIdx.x * kCtfThreads + tid;
-  double lsum = 0.0;
-  if (idx < H) {
-    const int ky = idx / Hx, kx = idx - ky * Hx;
-    const double idpx = 1.0 / ((double)D * (double)c.px), nyq = 1.0 / (2.0 * (double)c.px);
-    double fx[2], fy[2];
-    int nx = 1, ny = 1;
-    if (2 * kx == D) { fx[0] = nyq; fx[1] = -nyq; nx = 2; } else fx[0] = kx * idpx;
-    if (2 * ky == D) { fy[0] = nyq; fy[1] = -nyq; ny = 2; }
-    else fy[0] = (2 * ky < D ? ky : ky - D) * idpx;
+  const int D = c.D, Hx = D / 2 + 1, H = D * Hx;
+  const float gsc = 2.0f / ((float)D * (float)D), ps = 1.0f / ((float)D * (float)D);
+  float lsum = 0.f;
+  const int ky0 = blockIdx.x * kCtfRows, nb = Hx * kCtfRows;
+  const float invH = 1.f / (float)Hx;
+  for (int idx = tid; idx < nb; idx += kCtfThreads) {
+    const int r = (int)(((float)idx + 0.5f) * invH), kx = idx - r * Hx, ky = ky0 + r;
+    if (ky >= D) break;
+    const bool nx = 2 * kx == D, ny = 2 * ky == D;
+    const int kys = 2 * ky < D ? ky : ky - D;
+    // Nyquist bins average their +-1/(2 px) aliases (reading L12): sign flips of kx or ky
     float C = 0.f;
-    for (int a = 0; a < nx; ++a)
-      for (int b = 0; b < ny; ++b) C += ctf_raw(P, fx[a], fy[b]);
-    C *= 1.0f / (float)(nx * ny);
-    const size_t o = (size_t)i * H + idx;
+    const double kxd = kx, kyd = kys;
+    for (int a = 0; a < (nx ? 2 : 1); ++a)
+      for (int b2 = 0; b2 < (ny ? 2 : 1); ++b2) {
+        const double fx = a ? -kxd : kxd, fy = b2 ? -kyd : kyd;
+        C += ctf_raw(P, fx * fx + fy * fy, fx * fx - fy * fy, 2.0 * fx * fy);
+      }
+    if (nx || ny) C *= (nx && ny) ? 0.25f : 0.5f;
+    const size_t o = (size_t)i * H + (size_t)ky * Hx + kx;
     const float2 F = spec_hat[o], Ob = spec_obs[o];
     const float Rr = C * F.x - Ob.x, Ri = C * F.y - Ob.y;
-    const double wgt = (kx == 0 || 2 * kx == D) ? 1.0 : 2.0;
-    lsum = wgt * ((double)Rr * Rr + (double)Ri * Ri);
-    const float gsc = 2.0f / ((float)D * (float)D);
-    if (spec_pred) {
-      const float ps = 1.0f / ((float)D * (float)D);
-      spec_pred[o] = make_float2(C * F.x * ps, C * F.y * ps);
-    }
+    const float wgt = (kx == 0 || nx) ? 1.f : 2.f;
+    lsum = fmaf(wgt, fmaf(Rr, Rr, Ri * Ri), lsum);
+    if (spec_pred) spec_pred[o] = make_float2(C * F.x * ps, C * F.y * ps);
     spec_hat[o] = make_float2(gsc * C * Rr, gsc * C * Ri);
   }
+  double ls = lsum;
 #pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, d);
-  if ((tid & 31) == 0) red[tid >> 5] = lsum;
+  for (int d = 16; d >= 1; d >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, d);
+  if ((tid & 31) == 0) red[tid >> 5] = ls;
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
@@ -143,7 +151,7 @@ __global__ void __launch_bounds__(128) k_loss_reduce(int B, int nblk, const doub
 void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
                      float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches) {
   CtfP *P = reinterpret_cast<CtfP *>(ctf_par);
-  k_ctf_params<<<(B + 127) / 128, 128, 0, s>>>(B, ctf, P);
+  k_ctf_params<<<(B + 127) / 128, 128, 0, s>>>(B, 1.0 / ((double)c.D * (double)c.px), ctf, P);
   dim3 grid(loss_blocks, B);
   k_ctf_loss<<<grid, kCtfThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part);
   launches += 2;
@@ -157,6 +165,6 @@ void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double 
 
 size_t ctf_par_bytes() { return sizeof(CtfP); }
 
-int ctf_loss_blocks(int D) { return (D * (D / 2 + 1) + kCtfThreads - 1) / kCtfThreads; }
+int ctf_loss_blocks(int D) { return (D + kCtfRows - 1) / kCtfRows; }
 
 }  // namespace gem
