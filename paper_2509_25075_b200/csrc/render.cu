@@ -364,26 +364,27 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, const SplatR
 // Per-Gaussian reduction of the image-space slots over the particles of a launch, in a fixed
 // order (deterministic), transformed to world frame with W_i = P_i^T and added to acc:
 //   G_mu += W^T (l_mx, l_my, 0),  G_Sigma += W^T [G_hat 0; 0 0] W,  L_rho += q0 / rho.
-__global__ void __launch_bounds__(256) k_bwd_reduce(int B, int N,
-                                                    const float4 *__restrict__ slotA,
-                                                    const float2 *__restrict__ slotB,
-                                                    const float4 *__restrict__ mean_rho,
-                                                    const float *__restrict__ rot, float4 *__restrict__ acc) {
-  // thread (g, jl): Gaussian j = 64 blockIdx.x + jl, particles i = g, g + 4, ...; the four
-  // partial sums are combined in a fixed order (deterministic)
+constexpr int kRedG = 8, kRedJ = 32;   // particle groups x Gaussians per block
+
+__global__ void __launch_bounds__(kRedG * kRedJ) k_bwd_reduce(int B, int N, const float4 *__restrict__ slotA,
+                                                              const float2 *__restrict__ slotB,
+                                                              const float4 *__restrict__ mean_rho,
+                                                              const float *__restrict__ rot, float4 *__restrict__ acc) {
+  // thread (g, jl): Gaussian j = kRedJ blockIdx.x + jl, particles i = g, g + kRedG, ...; the
+  // kRedG partial sums are combined in a fixed order (deterministic)
   extern __shared__ float srot[];   // B x 6: rows 0 and 1 of W
-  __shared__ float part[3][10][64];
+  __shared__ float part[kRedG - 1][10][kRedJ];
   for (int k = threadIdx.x; k < 6 * B; k += blockDim.x) {
     const int i = k / 6, e = k % 6;
     srot[k] = rot[9 * i + 3 * (e % 3) + e / 3];   // W[row][col] = P[3 col + row], row = e / 3
   }
   __syncthreads();
-  const int jl = threadIdx.x & 63, g = threadIdx.x >> 6;
-  const int j = blockIdx.x * 64 + jl;
+  const int jl = threadIdx.x % kRedJ, g = threadIdx.x / kRedJ;
+  const int j = blockIdx.x * kRedJ + jl;
   float v[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (j < N) {
 #pragma unroll 4
-    for (int i = g; i < B; i += 4) {
+    for (int i = g; i < B; i += kRedG) {
       const size_t ij = (size_t)i * N + j;
       const float4 sa = __ldg(&slotA[ij]);
       const float2 sb = __ldg(&slotB[ij]);
@@ -411,7 +412,9 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(int B, int N,
   __syncthreads();
   if (g > 0 || j >= N) return;
 #pragma unroll
-  for (int k = 0; k < 10; ++k) v[k] = ((v[k] + part[0][k][jl]) + part[1][k][jl]) + part[2][k][jl];
+  for (int k = 0; k < 10; ++k)
+#pragma unroll
+    for (int gg = 0; gg < kRedG - 1; ++gg) v[k] += part[gg][k][jl];
   const float rho = mean_rho[j].w;
   float4 *dst = acc + 3 * (size_t)j;
   float4 a0 = dst[0], a1 = dst[1], a2 = dst[2];
@@ -459,7 +462,7 @@ void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float 
 
 void launch_bwd_reduce(const CfgDev &c, int B, const float4 *slotA, const float2 *slotB,
                        const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s, int &launches) {
-  k_bwd_reduce<<<(c.N + 63) / 64, 256, sizeof(float) * 6 * B, s>>>(B, c.N, slotA, slotB, mean_rho, rot, acc);
+  k_bwd_reduce<<<(c.N + kRedJ - 1) / kRedJ, kRedG * kRedJ, sizeof(float) * 6 * B, s>>>(B, c.N, slotA, slotB, mean_rho, rot, acc);
   ++launches;
 }
 
