@@ -203,6 +203,50 @@ class Trainer:
         return loss
 
 
+class HostPipeline:
+    """End-to-end training from pinned host batches through the public API: the inputs of step
+    k+1 are copied host->device on a side stream into the other half of a double buffer while
+    step k runs, and every step's loss is read back to pinned host memory.  Every input byte of
+    every step still crosses PCIe inside the caller's timed region; only the overlap is new."""
+
+    def __init__(self, trainer: "Trainer", B: int, D: int):
+        dev = trainer.params.t.device
+        self.tr = trainer
+        self.compute = trainer.step_ctx.stream
+        self.copy = torch.cuda.Stream(dev)
+        mk = lambda *shape: torch.empty(*shape, dtype=torch.float32, device=dev)
+        self.bufs = [(mk(B, 9), mk(B, 2), mk(B, 8), mk(B, D, D)) for _ in range(2)]
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.free = [torch.cuda.Event() for _ in range(2)]
+        self.used = [False, False]
+        self.loss_host = torch.empty(B + 1, dtype=torch.float64, pin_memory=True)
+
+    def _load(self, slot, batch):
+        with torch.cuda.stream(self.copy):
+            if self.used[slot]:
+                self.copy.wait_event(self.free[slot])   # step k-1 finished reading this buffer
+            for dst, src in zip(self.bufs[slot], batch):
+                dst.copy_(src, non_blocking=True)
+            self.ready[slot].record(self.copy)
+
+    def run(self, batches):
+        """batches: sequence of pinned host (rot [B,9], shift [B,2], ctf [B,8], observed [B,D,D]).
+        Returns the pinned host loss of the last step (valid after a stream sync)."""
+        n = len(batches)
+        self._load(0, batches[0])
+        for k in range(n):
+            slot = k % 2
+            if k + 1 < n:
+                self._load(1 - slot, batches[k + 1])
+            self.compute.wait_event(self.ready[slot])
+            loss = self.tr.train_step(*self.bufs[slot])
+            self.free[slot].record(self.compute)
+            self.used[slot] = True
+            with torch.cuda.stream(self.compute):
+                self.loss_host.copy_(loss, non_blocking=True)
+        return self.loss_host
+
+
 def allreduce_grad(grad: SoA, group=None):
     """Sum the [3, N, 4] gradient over the data-parallel ranks (one collective;
     NCCL over NVLink on GPUs, gloo on CPU tests).  No-op without a process group."""

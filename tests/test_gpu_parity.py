@@ -279,3 +279,28 @@ def test_workspace_has_no_cubic_term(gem):
         return L.gem_workspace_bytes(ctypes.byref(c))
     r = ws(256) / ws(128)
     assert r < 4.6, r    # quadratic at most (plus lists); D^3 would give 8
+
+
+def test_host_pipeline_matches_device_steps(gem):
+    """gem.HostPipeline (pinned host batches, double-buffered side-stream copies) must give the
+    same parameters, bit for bit, as the same training steps on device-resident inputs."""
+    case = make_case("T", B=3, seed=11)
+    w = case["w"]
+    B = 3
+    dev = torch.device("cuda", 0)
+    cfg = gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=B)
+    batches_np = []
+    for k in range(4):
+        rot, shift, ctf = synth.f32(*synth.particles(w, B, 100 + k))
+        obs = case["obs"] * np.float32(1.0 + 0.1 * k)
+        batches_np.append((rot, shift, ctf, obs))
+    P0 = gem.SoA.from_arrays(*case["params"], device=dev)
+    tr_a = gem.Trainer(cfg, gem.SoA(P0.t.clone()), dev)
+    for b in batches_np:
+        tr_a.train_step(*(torch.from_numpy(x).to(dev) for x in b))
+    tr_b = gem.Trainer(cfg, gem.SoA(P0.t.clone()), dev)
+    pipe = gem.HostPipeline(tr_b, B, w.D)
+    lh = pipe.run([[torch.from_numpy(x).pin_memory() for x in b] for b in batches_np])
+    torch.cuda.synchronize()
+    assert np.array_equal(tr_a.params.t.cpu().numpy(), tr_b.params.t.cpu().numpy())
+    assert np.isfinite(lh.numpy()).all() and lh[-1] > 0
