@@ -81,6 +81,7 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.rec = take(sizeof(SplatRec) * W * N);
   L.box = take(sizeof(uint2) * W * N);
   L.hist = take(sizeof(int) * (size_t)L.n_hist);
+  L.subcnt = take(sizeof(int) * (size_t)L.n_hist * 4);   // per fill-warp sub-chunk tile counts
   L.base = take(sizeof(int) * ((size_t)L.n_hist + 1));
   L.scan_blk = take(sizeof(int) * ((size_t)L.n_scan_blk + 1));
   L.ids = take(sizeof(int) * (size_t)L.list_cap);
@@ -356,10 +357,11 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     gem_status ps = plan_for(ctx, nb, &r2c, &c2r);
     if (ps != GEM_OK) return ps;
     const float *rw = rot + 9 * (size_t)p0;
-    { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist, st, s, ctx->launches); }
+    { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist, at<int>(ctx, L.subcnt), st, s,
+                         ctx->launches); }
     const int64_t nh = (int64_t)nb * c.NT * c.C;
     { Prof p(ctx, s, P_SCAN); launch_scan(hist, base, nh, at<int>(ctx, L.scan_blk), (nh + 4095) / 4096, st, c.cap, s, ctx->launches); }
-    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, ids, s, ctx->launches); }
+    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<int>(ctx, L.subcnt), ids, s, ctx->launches); }
     float *proj = proj_out ? proj_out + p0 * DD : at<float>(ctx, L.proj);
     { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, base, ids, proj, at<int>(ctx, L.ticket), s, ctx->launches); }
     CKF(cufftSetStream(r2c, s));

@@ -38,7 +38,7 @@ struct __align__(16) SplatRec {
 };
 
 struct Layout {  // byte offsets into the caller's workspace
-  size_t prep, rec, box, hist, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slot_a, slot_b, acc, loss_part, ctf_par,
+  size_t prep, rec, box, hist, subcnt, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slot_a, slot_b, acc, loss_part, ctf_par,
       stats, ticket, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, total;
   int64_t n_hist;       // B_max * NT * C
   int64_t n_scan_blk;
@@ -100,11 +100,12 @@ namespace gem {
 void launch_prep(const CfgDev &c, const float4 *log_scale, const float4 *quat, GaussPrep *prep, DevStats *st,
                  cudaStream_t s, int &launches);
 void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
-                        const float *shift, SplatRec *rec, uint2 *box, int *hist, DevStats *st, cudaStream_t s,
-                        int &launches);
+                        const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, DevStats *st,
+                        cudaStream_t s, int &launches);
 void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, DevStats *st, int64_t cap, cudaStream_t s,
                  int &launches);
-void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, int *ids, cudaStream_t s, int &launches);
+void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids, cudaStream_t s,
+                 int &launches);
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
                        int *ticket, cudaStream_t s, int &launches);
 void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, void *ctf_par, float2 *spec_hat, const float2 *spec_obs,

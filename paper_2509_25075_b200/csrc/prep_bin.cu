@@ -146,19 +146,23 @@ __device__ __noinline__ bool splat_exact(const GaussPrep &g, const double *W, do
 }
 
 constexpr int kSplatThreads = 256;
+constexpr int kFillWarps = 4, kSub = kChunk / kFillWarps;   // k_fill warps per chunk, Gaussians per warp
 
 __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, const GaussPrep *__restrict__ prep,
                                                                const float4 *__restrict__ mr,
                                                                const float *__restrict__ rot,
                                                                const float *__restrict__ shift,
                                                                SplatRec *__restrict__ rec, uint2 *__restrict__ box,
-                                                               int *__restrict__ hist, DevStats *__restrict__ st) {
-  extern __shared__ int shist[];   // [NT] tile histogram, then the exact-path queue [kChunk]
-  int *queue = shist + c.NT;
+                                                               int *__restrict__ hist, int *__restrict__ subcnt,
+                                                               DevStats *__restrict__ st) {
+  // [kFillWarps][NT] tile histograms of the chunk's kFillWarps sub-chunks (one per k_fill warp),
+  // then the exact-path queue [kChunk]
+  extern __shared__ int shist[];
+  int *queue = shist + kFillWarps * c.NT;
   __shared__ int qn;
   const int i = blockIdx.y, ch = blockIdx.x, tid = threadIdx.x;
   const GaussPrep32 *__restrict__ prep32 = reinterpret_cast<const GaussPrep32 *>(prep + c.N);
-  for (int t = tid; t < c.NT; t += blockDim.x) shist[t] = 0;
+  for (int t = tid; t < kFillWarps * c.NT; t += blockDim.x) shist[t] = 0;
   if (tid == 0) qn = 0;
   double W[9];
   float Wf[6];
@@ -182,8 +186,9 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
                          __int_as_float((vlo & 0xffff) | (vhi << 16)));
       pairs += (unsigned)((uhi - ulo + 1) * (vhi - vlo + 1));
       const int tu0 = (ulo >> c.tshift), tu1 = (uhi >> c.tshift), tv0 = (vlo >> c.tshift), tv1 = (vhi >> c.tshift);
+      int *sub = shist + ((j - ch * kChunk) / kSub) * c.NT;
       for (int tv = tv0; tv <= tv1; ++tv)
-        for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&shist[tv * c.nt + tu], 1);
+        for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&sub[tv * c.nt + tu], 1);
     } else {
       ulo = 1; uhi = 0; vlo = 1; vhi = 0;
       o.f0 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -257,7 +262,17 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
   for (int d = 16; d >= 1; d >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, d);
   if ((tid & 31) == 0 && pairs) atomicAdd(&st->pairs, (unsigned long long)pairs);
   __syncthreads();
-  for (int t = tid; t < c.NT; t += blockDim.x) hist[((size_t)i * c.NT + t) * c.C + ch] = shist[t];
+  int *sc = subcnt + ((size_t)i * c.C + ch) * kFillWarps * c.NT;
+  for (int t = tid; t < c.NT; t += blockDim.x) {
+    int tot = 0;
+#pragma unroll
+    for (int w = 0; w < kFillWarps; ++w) {
+      const int v = shist[w * c.NT + t];
+      sc[w * c.NT + t] = v;
+      tot += v;
+    }
+    hist[((size_t)i * c.NT + t) * c.C + ch] = tot;
+  }
 }
 
 // ------------------------------------------------------------------- scan
@@ -349,43 +364,25 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int *__restrict__ out
 // order within a tile's list is therefore (chunk, sub-chunk, step, slot, Gaussian id): a
 // deterministic function of the boxes (so the forward stays bitwise reproducible), and the
 // per-tile sets equal the oracle's (reading L9: only the set and its determinism matter).
-constexpr int kFillWarps = 4, kSub = kChunk / kFillWarps;
 
-__device__ __forceinline__ void rect_of(uint2 b, int ts, int &tu0, int &tu1, int &tv0, int &n) {
-  const int ulo = (int)(b.x & 0xffff), uhi = (int)(b.x >> 16), vlo = (int)(b.y & 0xffff), vhi = (int)(b.y >> 16);
-  if (ulo <= uhi && vlo <= vhi) {
-    tu0 = ulo >> ts; tu1 = uhi >> ts; tv0 = vlo >> ts;
-    n = (tu1 - tu0 + 1) * ((vhi >> ts) - tv0 + 1);
-  } else {
-    tu0 = 0; tu1 = -1; tv0 = 0; n = 0;
-  }
-}
 
 __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 *__restrict__ box,
-                                                          const int *__restrict__ base, int *__restrict__ ids) {
-  extern __shared__ int cnt[];   // [kFillWarps][NT]
+                                                          const int *__restrict__ base,
+                                                          const int *__restrict__ subcnt, int *__restrict__ ids) {
+  extern __shared__ int cnt[];   // [kFillWarps][NT] cursors
   const int i = blockIdx.y, ch = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int *mine = cnt + w * c.NT;
-  for (int t = threadIdx.x; t < kFillWarps * c.NT; t += blockDim.x) cnt[t] = 0;
-  __syncthreads();
   const int jsub = ch * kChunk + w * kSub;
   const uint2 *boxi = box + (size_t)i * c.N;
-  for (int j = jsub + lane; j < min(jsub + kSub, c.N); j += 32) {   // pass 1: per-tile counts
-    const uint2 b = boxi[j];
-    const int ulo = (int)(b.x & 0xffff), uhi = (int)(b.x >> 16), vlo = (int)(b.y & 0xffff), vhi = (int)(b.y >> 16);
-    if (ulo > uhi || vlo > vhi) continue;
-    const int tu0 = (ulo >> c.tshift), tu1 = (uhi >> c.tshift), tv1 = (vhi >> c.tshift);
-    for (int tv = (vlo >> c.tshift); tv <= tv1; ++tv)
-      for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&mine[tv * c.nt + tu], 1);
-  }
-  __syncthreads();
+  // cursors: the chunk's offset of each tile plus the counts of the preceding sub-chunks (the
+  // splat kernel counted each sub-chunk's entries per tile)
+  const int *sc = subcnt + ((size_t)i * c.C + ch) * kFillWarps * c.NT;
   for (int t = threadIdx.x; t < c.NT; t += blockDim.x) {
     int run = base[((size_t)i * c.NT + t) * c.C + ch];
 #pragma unroll
     for (int ww = 0; ww < kFillWarps; ++ww) {
-      const int v = cnt[ww * c.NT + t];
       cnt[ww * c.NT + t] = run;
-      run += v;
+      run += sc[ww * c.NT + t];
     }
   }
   __syncthreads();
@@ -394,9 +391,15 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
     const int j0 = jsub + step * 32;
     if (j0 >= c.N) break;
     const int j = j0 + lane;
-    int tu0 = 0, tu1 = -1, tv0 = 0, n = 0;
-    if (j < c.N) rect_of(boxi[j], c.tshift, tu0, tu1, tv0, n);
-    const int ntu = tu1 - tu0 + 1, ntv = n > 0 ? n / max(ntu, 1) : 0;
+    int tu0 = 0, tv0 = 0, ntu = 0, ntv = 0;
+    if (j < c.N) {
+      const uint2 b = boxi[j];
+      const int ulo = (int)(b.x & 0xffff), uhi = (int)(b.x >> 16), vlo = (int)(b.y & 0xffff), vhi = (int)(b.y >> 16);
+      if (ulo <= uhi && vlo <= vhi) {
+        tu0 = ulo >> c.tshift; tv0 = vlo >> c.tshift;
+        ntu = (uhi >> c.tshift) - tu0 + 1; ntv = (vhi >> c.tshift) - tv0 + 1;
+      }
+    }
     // slot-major order: every lane's tile (dv, du) of its rectangle, (dv, du) ascending, then lane
     const int mu = __reduce_max_sync(0xffffffffu, (unsigned)max(ntu, 0));
     const int mv = __reduce_max_sync(0xffffffffu, (unsigned)ntv);
@@ -427,16 +430,16 @@ void launch_prep(const CfgDev &c, const float4 *log_scale, const float4 *quat, G
 }
 
 void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
-                        const float *shift, SplatRec *rec, uint2 *box, int *hist, DevStats *st, cudaStream_t s,
-                        int &launches) {
+                        const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, DevStats *st,
+                        cudaStream_t s, int &launches) {
   dim3 grid(c.C, B);
-  const size_t smem = (c.NT + kChunk) * sizeof(int);
+  const size_t smem = (kFillWarps * c.NT + kChunk) * sizeof(int);
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(k_splat_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     init = true;
   }
-  k_splat_count<<<grid, kSplatThreads, smem, s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, st);
+  k_splat_count<<<grid, kSplatThreads, smem, s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, subcnt, st);
   ++launches;
 }
 
@@ -448,11 +451,12 @@ void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, Dev
   launches += 3;
 }
 
-void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, int *ids, cudaStream_t s, int &launches) {
+void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids, cudaStream_t s,
+                 int &launches) {
   dim3 grid(c.C, B);
   const size_t smem = (size_t)kFillWarps * c.NT * sizeof(int);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_fill<<<grid, kFillWarps * 32, smem, s>>>(c, box, base, ids);
+  k_fill<<<grid, kFillWarps * 32, smem, s>>>(c, box, base, subcnt, ids);
   ++launches;
 }
 
