@@ -53,18 +53,22 @@ __device__ __forceinline__ void retire(int *ticket, int lane) {
 
 // Forward kernel.  Register accumulators: lane L owns row pair p = L / NCP of the tile
 // (NCP = 32 / NP lanes per pair) and keeps a private copy of that pair-row, T columns x 2 rows,
-// in registers.  Per chunk of <= kCH entries, each lane takes one entry, computes its constants
-// and the start values of its row-pair segments (vertical recurrence) and appends each segment
-// to the bin of its row pair (ballots, in list order: deterministic).  Then the NCP lanes of
-// pair p take the segments of bin p round-robin and render each one with a fully unrolled,
-// predicated T-column recurrence into their registers: no shared-memory read-modify-write,
-// no divergence from box widths.  At the end the NCP copies of each pair-row are summed by a
-// fixed butterfly of shuffles (bitwise deterministic).
+// in registers.  Per chunk of <= kCH entries, each lane takes one entry (records prefetched one
+// 32-entry group ahead, ids two), stores its per-entry constants once in shared memory and
+// appends the entry's index to the bin of every row pair its box covers (ballots, in list
+// order: deterministic).  Then the NCP lanes of pair p take the segments of bin p round-robin:
+// a lane evaluates its segment's start values directly (e and the row ratio R at the first
+// column of rows 2p and 2p+1: four exps) and renders the segment with a fully unrolled,
+// predicated T-column recurrence into its registers: no shared-memory read-modify-write and no
+// divergence from box widths.  At the end the NCP copies of each pair-row are summed by a fixed
+// butterfly of shuffles (bitwise deterministic).
 template <int T>
 struct FwdSmem {
   static constexpr int NP = T / 2;
-  float4 sA[NP][kCH];   // fast: (eA, eB, RA, RB) at column cu0; slow: (fA, fB, gA, gB)
-  float2 sB[NP][kCH];   // (S or na, bits = cu0 | cu1 << 8 | vA << 16 | vB << 17 | slow << 31)
+  float4 eA[kCH];                // (my, nb2, nc, amp)           tile-local pixel units, log2 scale
+  float4 eB[kCH];                // (Fx, Gx, D0, S = 2^{2 na})   f(dx0, dy) = Fx + dy (Gx + nc dy)
+  float2 eC[kCH];                // (na, bits)  bits = cu0 | cu1 << 8 | cv0 << 16 | cv1 << 24 | slow << 31
+  unsigned char bin[NP][kCH];    // entry indices per row pair
 };
 
 template <int T>
@@ -80,6 +84,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
   SM &sm = reinterpret_cast<SM *>(fwd_dsm)[w];
   const unsigned lt = (1u << lane) - 1u;
   const int mp = lane / NCP, cp = lane % NCP;
+  const float pyA = (float)(2 * mp);
   const int items = B * c.NT;
   for (;;) {
     const int item = next_item(ticket, lane);
@@ -110,70 +115,39 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
     if (lane < nall) nxt = reci[id1];
     int blen = 0;   // length of bin mp in the current chunk (lanes of pair pp hold bin pp's length)
     for (int g0 = 0; g0 < nall; g0 += 32) {
-      const int q = g0 + lane;
+      const int q = g0 + lane, qc = g0 % kCH + lane;   // list position, index within the chunk
       const SplatRec rr = nxt;
       if (q + 32 < nall) nxt = reci[id2];
       if (q + 64 < nall) id2 = ids[s + q + 64];
-      {
-        int pr0 = NP, pr1 = -1, cu0 = 0, cu1 = 0, cv0 = 0, cv1 = 0;
-        bool slow = false, neg = false;
-        float El = 0.f, V = 0.f, Rl = 0.f, W = 0.f, Kb = 0.f, S = 0.f, na = 0.f, nb2 = 0.f, nc = 0.f, Fx = 0.f,
-              Gx = 0.f, D0 = 0.f, my = 0.f, la = 0.f;
-        if (q < nall) {
-          const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
-          const int ulo = (ub & 0xffff) - u0, uhi = (ub >> 16) - u0, vlo = (vb & 0xffff) - v0, vhi = (vb >> 16) - v0;
-          cu0 = max(ulo, 0); cu1 = min(uhi, T - 1); cv0 = max(vlo, 0); cv1 = min(vhi, T - 1);
-          pr0 = cv0 >> 1; pr1 = cv1 >> 1;
-          na = nh * rr.f0.z; nb2 = 2.f * nh * rr.f0.w; nc = nh * rr.f1.x;
-          const float mx = (float)ulo + rr.f0.x;
-          my = (float)vlo + rr.f0.y;
-          const float dx0 = (float)cu0 - mx;
-          Fx = na * dx0 * dx0; Gx = nb2 * dx0; D0 = na * fmaf(2.f, dx0, 1.f);
-          const float d0 = (float)cv0 - my, d1 = (float)cv1 - my;
-          const float f0 = fmaf(d0, fmaf(nc, d0, Gx), Fx), f1 = fmaf(d1, fmaf(nc, d1, Gx), Fx);
-          const float r0 = fmaf(nb2, d0, D0), r1 = fmaf(nb2, d1, D0);
-          slow = !(fminf(f0, f1) >= -100.f && fminf(r0, r1) >= -120.f && nc >= -60.f && fabsf(nb2) <= 120.f);
-          const float amp = rr.f1.y;
-          S = ex2(2.f * na);
-          W = ex2(2.f * nc);
-          Kb = ex2(nb2);
-          El = amp * ex2(f0);
-          V = ex2(fmaf(nc, fmaf(2.f, d0, 1.f), Gx));
-          Rl = ex2(r0);
-          la = __log2f(fabsf(amp));
-          neg = amp < 0.f;
-          if (neg) slow = true;   // the direct path carries the sign
-        }
-        const int sbits = cu0 | (cu1 << 8) | (slow ? (int)0x80000000 : 0) | (neg ? 1 << 18 : 0);
+      int pr0 = NP, pr1 = -1;
+      if (q < nall) {
+        const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
+        const int ulo = (ub & 0xffff) - u0, uhi = (ub >> 16) - u0, vlo = (vb & 0xffff) - v0, vhi = (vb >> 16) - v0;
+        const int cu0 = max(ulo, 0), cu1 = min(uhi, T - 1), cv0 = max(vlo, 0), cv1 = min(vhi, T - 1);
+        pr0 = cv0 >> 1;
+        pr1 = cv1 >> 1;
+        const float na = nh * rr.f0.z, nb2 = 2.f * nh * rr.f0.w, nc = nh * rr.f1.x;
+        const float mx = (float)ulo + rr.f0.x, my = (float)vlo + rr.f0.y;
+        const float dx0 = (float)cu0 - mx;
+        const float Fx = na * dx0 * dx0, Gx = nb2 * dx0, D0 = na * fmaf(2.f, dx0, 1.f);
+        // the recurrence needs its factors normal: first-column values and the row ratio at the
+        // covered rows (f concave, ratio linear in dy: check the end rows) and the amplitude sign
+        const float d0 = (float)cv0 - my, d1 = (float)cv1 - my;
+        const float f0 = fmaf(d0, fmaf(nc, d0, Gx), Fx), f1 = fmaf(d1, fmaf(nc, d1, Gx), Fx);
+        const float r0 = fmaf(nb2, d0, D0), r1 = fmaf(nb2, d1, D0);
+        const bool slow = !(fminf(f0, f1) >= -100.f && fminf(r0, r1) >= -120.f && rr.f1.y > 0.f);
+        sm.eA[qc] = make_float4(my, nb2, nc, rr.f1.y);
+        sm.eB[qc] = make_float4(Fx, Gx, D0, ex2(2.f * na));
+        sm.eC[qc] = make_float2(na, __int_as_float(cu0 | (cu1 << 8) | (cv0 << 16) | (cv1 << 24) |
+                                                   (slow ? (int)0x80000000 : 0)));
+      }
 #pragma unroll
-        for (int pp = 0; pp < NP; ++pp) {
-          const bool in = pr0 <= pp && pp <= pr1;
-          const bool vA = in && 2 * pp >= cv0, vB = in && 2 * pp + 1 <= cv1;
-          float4 sa;
-          float2 sb;
-          if (!slow) {
-            sa.x = vA ? El : 0.f;
-            sa.z = vA ? Rl : 0.f;
-            if (vA) { El *= V; V *= W; Rl *= Kb; }
-            sa.y = vB ? El : 0.f;
-            sa.w = vB ? Rl : 0.f;
-            if (vB) { El *= V; V *= W; Rl *= Kb; }
-            sb = make_float2(S, __int_as_float(sbits));
-          } else {
-            const float dA = (float)(2 * pp) - my, dB = dA + 1.f;
-            sa = make_float4(fmaf(dA, fmaf(nc, dA, Gx), Fx) + la, fmaf(dB, fmaf(nc, dB, Gx), Fx) + la,
-                             fmaf(nb2, dA, D0), fmaf(nb2, dB, D0));
-            sb = make_float2(na, __int_as_float(sbits | (vA ? 1 << 16 : 0) | (vB ? 1 << 17 : 0)));
-          }
-          const unsigned bal = __ballot_sync(0xffffffffu, in);
-          const int before = __shfl_sync(0xffffffffu, blen, pp * NCP);
-          if (in) {
-            const int pos = before + __popc(bal & lt);
-            sm.sA[pp][pos] = sa;
-            sm.sB[pp][pos] = sb;
-          }
-          if (mp == pp) blen += __popc(bal);
-        }
+      for (int pp = 0; pp < NP; ++pp) {
+        const bool in = pr0 <= pp && pp <= pr1;
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        const int before = __shfl_sync(0xffffffffu, blen, pp * NCP);
+        if (in) sm.bin[pp][before + __popc(bal & lt)] = (unsigned char)qc;
+        if (mp == pp) blen += __popc(bal);
       }
       if ((g0 + 32) % kCH != 0 && g0 + 32 < nall) continue;   // the chunk's bins are not full yet
       __syncwarp();
@@ -181,13 +155,19 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
 #pragma unroll 1
       for (int sg = cp; __any_sync(0xffffffffu, sg < blen); sg += NCP) {
         if (sg >= blen) continue;
-        const float4 A = sm.sA[mp][sg];
-        const float2 Bv = sm.sB[mp][sg];
-        const int bits = __float_as_int(Bv.y);
-        const int k0 = bits & 0xff, k1 = (bits >> 8) & 0xff;
+        const int qe = sm.bin[mp][sg];
+        const float4 A = sm.eA[qe], Bq = sm.eB[qe];
+        const float2 Cq = sm.eC[qe];
+        const int bits = __float_as_int(Cq.y);
+        const int k0 = bits & 0xff, k1 = (bits >> 8) & 0xff, cv0 = (bits >> 16) & 0xff, cv1 = (bits >> 24) & 0x7f;
+        const bool vA = 2 * mp >= cv0, vB = 2 * mp + 1 <= cv1;
+        const float dyA = pyA - A.x, dyB = dyA + 1.f, nb2 = A.y, nc = A.z, amp = A.w;
+        const float fA = fmaf(dyA, fmaf(nc, dyA, Bq.y), Bq.x), fB = fmaf(dyB, fmaf(nc, dyB, Bq.y), Bq.x);
+        const float gA = fmaf(nb2, dyA, Bq.z), gB = gA + nb2;   // log2 R at the first column
         if (bits >= 0) {
-          float2 E2 = make_float2(A.x, A.y), R2 = make_float2(A.z, A.w);
-          const float2 S2 = make_float2(Bv.x, Bv.x);
+          float2 E2 = make_float2(vA ? amp * ex2(fA) : 0.f, vB ? amp * ex2(fB) : 0.f);
+          float2 R2 = make_float2(vA ? ex2(gA) : 0.f, vB ? ex2(gB) : 0.f);
+          const float2 S2 = make_float2(Bq.w, Bq.w);
 #pragma unroll
           for (int k = 0; k < T; ++k) {
             if (k >= k0 && k <= k1) {
@@ -197,14 +177,13 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
             }
           }
         } else {   // direct evaluation: f = f0 + kk g0 + kk (kk - 1) na, kk = k - k0
-          const float sg1 = (bits & (1 << 18)) ? -1.f : 1.f;
-          const bool vA = bits & (1 << 16), vB = bits & (1 << 17);
+          const float na = Cq.x;
 #pragma unroll
           for (int k = 0; k < T; ++k) {
             if (k >= k0 && k <= k1) {
-              const float kf = (float)(k - k0), kq = kf * (kf - 1.f) * Bv.x;
-              if (vA) acc[k].x += sg1 * ex2(fmaf(kf, A.z, A.x) + kq);
-              if (vB) acc[k].y += sg1 * ex2(fmaf(kf, A.w, A.y) + kq);
+              const float kf = (float)(k - k0), kq = kf * (kf - 1.f) * na;
+              if (vA) acc[k].x = fmaf(amp, ex2(fmaf(kf, gA, fA) + kq), acc[k].x);
+              if (vB) acc[k].y = fmaf(amp, ex2(fmaf(kf, gB, fB) + kq), acc[k].y);
             }
           }
         }
