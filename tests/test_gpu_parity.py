@@ -304,3 +304,47 @@ def test_host_pipeline_matches_device_steps(gem):
     torch.cuda.synchronize()
     assert np.array_equal(tr_a.params.t.cpu().numpy(), tr_b.params.t.cpu().numpy())
     assert np.isfinite(lh.numpy()).all() and lh[-1] > 0
+
+
+def test_R_config_full_size(gem, orc):
+    """BASELINE config R at full size (N = 50,000, D = 256, px = 1.31 A) in the bench's launch
+    configuration (default 8x8 tiles, non-fused), one particle: bit-exact lists and the whole
+    projection, prediction, loss and every gradient class against the un-culled fp64 oracle
+    (~3e9 Gaussian-pixel terms per pass on the host cores)."""
+    case = make_case("R", B=1, seed=12)
+    g = run_gpu(gem, case, tile=8, want_lists=True)
+    assert g["stats"]["status"] == 0, g["stats"]
+    assert_lists_exact(orc, case, g["lists"], 8)
+    o = oracle_out(orc, case)
+    assert maxnorm_rel(g["proj"][0], o["proj"][0]) < IMG_TOL
+    assert maxnorm_rel(g["pred"][0], o["pred"][0]) < IMG_TOL
+    assert abs(g["loss"][-1] - o["total"]) < LOSS_TOL * o["total"]
+    for name, cols in CLASSES.items():
+        assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+
+
+def test_R_config_bench_batch_sampled(gem, orc):
+    """The bench's exact launch configuration (config R, B = 128 particles per step, 8x8 tiles):
+    lists, projection and per-particle loss of three sampled particles against the oracle, and a
+    property for the summed gradient that holds at any size: the batch gradient equals the sum
+    of the gradients of its four 32-particle quarters."""
+    B = 128
+    case = make_case("R", B=B, seed=13)
+    g = run_gpu(gem, case, tile=8)
+    assert g["stats"]["status"] == 0, g["stats"]
+    st = g["st"]
+    for i in (0, 63, 127):
+        sub = dict(case, rot=case["rot"][i:i + 1], shift=case["shift"][i:i + 1], ctf=case["ctf"][i:i + 1],
+                   obs=case["obs"][i:i + 1])
+        assert_lists_exact(orc, sub, [st.export_lists(i)], 8)
+        o = oracle_out(orc, sub, want=("proj",))
+        assert maxnorm_rel(g["proj"][i], o["proj"][0]) < IMG_TOL
+        assert abs(g["loss"][i] - o["total"]) < LOSS_TOL * o["total"]
+    parts = []
+    for q in range(4):
+        sl = slice(32 * q, 32 * q + 32)
+        sub = dict(case, rot=case["rot"][sl], shift=case["shift"][sl], ctf=case["ctf"][sl], obs=case["obs"][sl])
+        parts.append(run_gpu(gem, sub, tile=8)["grad"].astype(np.float64))
+    tot = sum(parts)
+    for name, cols in CLASSES.items():
+        assert maxnorm_rel(g["grad"][:, cols], tot[:, cols]) < 1e-5, name
