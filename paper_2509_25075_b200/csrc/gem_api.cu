@@ -103,6 +103,7 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.stage_obs = take(sizeof(float) * Bm * D * D);
   L.stage_loss = take(sizeof(double) * (Bm + 1));
   L.cufft_work = take(cufft_bytes);
+  L.cufft_work2 = take(cufft_bytes);
   L.total = o;
   return L;
 }
@@ -130,37 +131,46 @@ bool soa_aligned(const gem_soa *s) {
   return aligned16(s->mean_rho) && aligned16(s->log_scale) && aligned16(s->quat);
 }
 
-gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r) {
+gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r, cufftHandle *r2c_obs) {
   for (int k = 0; k < ctx->n_plans; ++k)
-    if (ctx->plan_B[k] == B) { *r2c = ctx->plan_r2c[k]; *c2r = ctx->plan_c2r[k]; return GEM_OK; }
+    if (ctx->plan_B[k] == B) {
+      *r2c = ctx->plan_r2c[k];
+      *c2r = ctx->plan_c2r[k];
+      *r2c_obs = ctx->plan_obs[k];
+      return GEM_OK;
+    }
   int slot = ctx->n_plans < 8 ? ctx->n_plans : 7;
   if (ctx->n_plans >= 8) {  // evict the last slot
     cufftDestroy(ctx->plan_r2c[7]);
     cufftDestroy(ctx->plan_c2r[7]);
+    cufftDestroy(ctx->plan_obs[7]);
     ctx->n_plans = 7;
   }
-  size_t wa = 0, wb = 0;
-  cufftHandle a, b;
+  size_t wa = 0, wb = 0, wc = 0;
+  cufftHandle a, b, o;
   if (!make_plan(ctx->dc.D, B, CUFFT_R2C, &a, &wa)) return GEM_E_CUFFT;
   if (!make_plan(ctx->dc.D, B, CUFFT_C2R, &b, &wb)) { cufftDestroy(a); return GEM_E_CUFFT; }
-  if (wa > ctx->L.cufft_bytes || wb > ctx->L.cufft_bytes) { cufftDestroy(a); cufftDestroy(b); return GEM_E_CUFFT; }
-  void *work = ctx->ws + ctx->L.cufft_work;
-  if (cufftSetWorkArea(a, work) != CUFFT_SUCCESS || cufftSetWorkArea(b, work) != CUFFT_SUCCESS) {
-    cufftDestroy(a); cufftDestroy(b);
+  if (!make_plan(ctx->dc.D, B, CUFFT_R2C, &o, &wc)) { cufftDestroy(a); cufftDestroy(b); return GEM_E_CUFFT; }
+  const size_t cap = ctx->L.cufft_bytes;
+  void *work = ctx->ws + ctx->L.cufft_work, *work2 = ctx->ws + ctx->L.cufft_work2;
+  if (wa > cap || wb > cap || wc > cap || cufftSetWorkArea(a, work) != CUFFT_SUCCESS ||
+      cufftSetWorkArea(b, work) != CUFFT_SUCCESS || cufftSetWorkArea(o, work2) != CUFFT_SUCCESS) {
+    cufftDestroy(a); cufftDestroy(b); cufftDestroy(o);
     return GEM_E_CUFFT;
   }
   ctx->plan_B[slot] = B;
   ctx->plan_r2c[slot] = a;
   ctx->plan_c2r[slot] = b;
+  ctx->plan_obs[slot] = o;
   ctx->n_plans = slot + 1;
   *r2c = a;
   *c2r = b;
+  *r2c_obs = o;
   return GEM_OK;
 }
 
-// ---- profiling: an event pair around each launch group while enabled
 const char *kProfNames[P_COUNT] = {"prep", "splat_count", "scan", "fill", "render_fwd", "fft_r2c",
-                                   "ctf_loss", "fft_c2r", "render_bwd", "bwd_reduce", "finalize", "adam", "volume"};
+                                   "ctf_loss", "fft_c2r", "fft_r2c_obs", "render_bwd", "bwd_reduce", "finalize", "adam", "volume"};
 
 struct Prof {
   gem_ctx *ctx;
@@ -247,9 +257,15 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
   ctx->n_plans = 0;
   ctx->W = c.wave;
   ctx->fused = (c.flags & GEM_FLAG_FUSED) ? 1 : 0;
-  cufftHandle a, b;
-  gem_status st = plan_for(ctx, c.wave, &a, &b);
-  if (st != GEM_OK) { delete ctx; return st; }
+  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    delete ctx;
+    return GEM_E_CUDA;
+  }
+  cufftHandle a, b, o;
+  gem_status st = plan_for(ctx, c.wave, &a, &b, &o);
+  if (st != GEM_OK) { gem_destroy(ctx); return st; }
   if (cudaMemsetAsync(ctx->ws + L.stats, 0, sizeof(DevStats), ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(ctx->ws + L.ticket, 0, 64, ctx->stream) != cudaSuccess ||
       cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
@@ -266,6 +282,13 @@ gem_status gem_destroy(gem_ctx *ctx) {
   for (int k = 0; k < ctx->n_plans; ++k) {
     cufftDestroy(ctx->plan_r2c[k]);
     cufftDestroy(ctx->plan_c2r[k]);
+    cufftDestroy(ctx->plan_obs[k]);
+  }
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+    cudaEventDestroy(ctx->ev_fork);
+    cudaEventDestroy(ctx->ev_join);
   }
   for (int k = 0; k < 2 * ctx->prof_cap; ++k) cudaEventDestroy(ctx->prof_ev[k]);
   free(ctx->prof_ev);
@@ -353,9 +376,19 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
   int p0 = 0, nb = 0;
   for (p0 = 0; p0 < B; p0 += ctx->W) {   // one wave (all of B when not fused)
     nb = B - p0 < ctx->W ? B - p0 : ctx->W;
-    cufftHandle r2c, c2r;
-    gem_status ps = plan_for(ctx, nb, &r2c, &c2r);
+    cufftHandle r2c, c2r, r2c_obs;
+    gem_status ps = plan_for(ctx, nb, &r2c, &c2r, &r2c_obs);
     if (ps != GEM_OK) return ps;
+    // fork: the observed images' R2C runs on the internal side stream, overlapped with the
+    // splat / binning / render of this wave; joined before the CTF/loss kernel
+    CK(cudaEventRecord(ctx->ev_fork, s));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    CKF(cufftSetStream(r2c_obs, ctx->side));
+    {
+      Prof p(ctx, ctx->side, P_FFT_OBS);
+      CKF(cufftExecR2C(r2c_obs, (cufftReal *)(obs + p0 * DD), (cufftComplex *)so));
+    }
+    CK(cudaEventRecord(ctx->ev_join, ctx->side));
     const float *rw = rot + 9 * (size_t)p0;
     { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist, at<int>(ctx, L.subcnt), st, s,
                          ctx->launches); }
@@ -369,8 +402,8 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     {
       Prof p(ctx, s, P_FFT_R2C);
       CKF(cufftExecR2C(r2c, (cufftReal *)proj, (cufftComplex *)sh));
-      CKF(cufftExecR2C(r2c, (cufftReal *)(obs + p0 * DD), (cufftComplex *)so));
     }
+    CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     {
       Prof p(ctx, s, P_CTF_LOSS);
       launch_ctf_loss(c, nb, ctf + 8 * (size_t)p0, ctx->ws + L.ctf_par, sh, so, pred_out ? sp : nullptr, lpart + (size_t)p0 * L.loss_blocks,

@@ -39,7 +39,7 @@ struct __align__(16) SplatRec {
 
 struct Layout {  // byte offsets into the caller's workspace
   size_t prep, rec, box, hist, subcnt, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slot_a, slot_b, acc, loss_part, ctf_par,
-      stats, ticket, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, total;
+      stats, ticket, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, cufft_work2, total;
   int64_t n_hist;       // B_max * NT * C
   int64_t n_scan_blk;
   int64_t list_cap;
@@ -75,7 +75,9 @@ struct gem_ctx {
   cudaStream_t stream;
   // cuFFT plans keyed by batch size (small cache)
   int plan_B[8];
-  cufftHandle plan_r2c[8], plan_c2r[8];
+  cufftHandle plan_r2c[8], plan_c2r[8], plan_obs[8];   // plan_obs: R2C of the observed images (side stream)
+  cudaStream_t side;   // internal stream: observed-image R2C overlapped with splat/bin/render
+  cudaEvent_t ev_fork, ev_join;
   int n_plans;
   int fwd_live;        // a forward's lists/records/dL/dI are valid
   int last_B;
@@ -91,7 +93,7 @@ struct gem_ctx {
 };
 
 namespace gem {
-enum ProfKind { P_PREP, P_SPLAT, P_SCAN, P_FILL, P_RENDER_FWD, P_FFT_R2C, P_CTF_LOSS, P_FFT_C2R, P_RENDER_BWD,
+enum ProfKind { P_PREP, P_SPLAT, P_SCAN, P_FILL, P_RENDER_FWD, P_FFT_R2C, P_CTF_LOSS, P_FFT_C2R, P_FFT_OBS, P_RENDER_BWD,
                 P_BWD_REDUCE, P_FINALIZE, P_ADAM, P_VOLUME, P_COUNT };
 }
 
