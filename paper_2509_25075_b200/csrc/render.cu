@@ -86,13 +86,27 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
   const int mp = lane / NCP, cp = lane % NCP;
   const float pyA = (float)(2 * mp);
   const int items = B * c.NT;
+  // item pipeline: the next item's ticket and list bounds are fetched while the current item is
+  // processed (hides the global atomic and the two dependent loads)
+  auto bounds = [&](int it, int &s_, int &e_) {
+    s_ = 0; e_ = 0;
+    if (it < items) {
+      const int ii = it / c.NT, tt = it - ii * c.NT;
+      const size_t h = ((size_t)ii * c.NT + tt) * c.C;
+      s_ = base[h];
+      e_ = base[h + c.C];
+    }
+  };
+  int nitem = next_item(ticket, lane), ns, ne;
+  bounds(nitem, ns, ne);
   for (;;) {
-    const int item = next_item(ticket, lane);
+    const int item = nitem;
     if (item >= items) break;
+    int s = ns, e = ne;
+    nitem = next_item(ticket, lane);
+    bounds(nitem, ns, ne);
     const int i = item / c.NT, t = item - i * c.NT;
     const int u0 = (t % c.nt) * T, v0 = (t / c.nt) * T;
-    const size_t hidx = ((size_t)i * c.NT + t) * c.C;
-    int s = base[hidx], e = base[hidx + c.C];
     if ((int64_t)e > c.cap) e = (int)c.cap;
     if ((int64_t)s > c.cap) s = (int)c.cap;
     float *out = proj + (size_t)i * c.D * c.D;
