@@ -68,6 +68,15 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def measured_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (profiles/traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p))[kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def fp32_peak_tflops(sm_mhz):
     """148 SMs x 128 FP32 lanes x 2 FLOP/FMA x clock (B200_PROFILING.md unit counts)."""
     return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
@@ -330,7 +339,7 @@ def main():
         achieved = per_pair * pairs * args.steps / (kern[dominant][1] / 1e3) / 1e12
         peak = fp32_peak_tflops(sm_max)
         roof = {"bound": "alu", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": measured_traffic(dominant),
                 "work_per_launch": f"{per_pair} FP32 FLOP x {pairs} useful (Gaussian, pixel) pairs per step, "
                                    f"{kern[dominant][0] // max(args.steps, 1)} launch(es) per step",
                 "avg_launch_ms": avg_s * 1e3,

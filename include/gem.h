@@ -90,10 +90,15 @@ typedef struct {
  * of `wave` particles, running splat -> cull/bin -> projection -> FFT/CTF/loss
  * -> C2R -> backward scatter per wave so that splat records, tile lists and
  * images stay resident in L2; gem_backward then only finalizes the gradient
- * from the accumulators.  Results are those of the unfused path (same
- * arithmetic; the scatter's atomic order differs).  In fused mode
+ * from the accumulators.  Results equal the unfused path's up to the
+ * summation order over waves (every path is deterministic).  In fused mode
  * gem_export_lists can only export particles of the last wave. */
-enum { GEM_FLAG_FUSED = 1 };
+/* Ablation variants of the paper's Table 5:
+ * GEM_FLAG_NO_ROTATION  "No Rotation, fix R_i = I": gem_step writes q = (1, 0, 0, 0) and the
+ *                       quaternion gradient from gem_backward is exactly zero.
+ * GEM_FLAG_ISOTROPIC    "Isotropic Scaling": after every gem_step the three log-scales of each
+ *                       Gaussian are set to their mean (S:361 reading). */
+enum { GEM_FLAG_FUSED = 1, GEM_FLAG_NO_ROTATION = 2, GEM_FLAG_ISOTROPIC = 4 };
 
 /* Gaussian parameter store (a0): three float4 arrays of length N.
  *   mean_rho [N] = (mu_x, mu_y, mu_z [Angstrom], rho)

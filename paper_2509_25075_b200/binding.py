@@ -16,6 +16,8 @@ GEM_OK, GEM_E_INVALID, GEM_E_SHAPE, GEM_E_ALIGN, GEM_E_CUDA, GEM_E_CUFFT, GEM_E_
     GEM_E_NONFINITE = range(9)
 GEM_MEM_DEVICE, GEM_MEM_HOST = 0, 1
 GEM_FLAG_FUSED = 1
+GEM_FLAG_NO_ROTATION = 2   # Table 5 ablation: R fixed to I
+GEM_FLAG_ISOTROPIC = 4     # Table 5 ablation: tied log-scales
 
 
 class GemConfigC(ctypes.Structure):

@@ -36,7 +36,8 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   d.px = c.pixel_size;
   d.k = c.cull_k;
   d.tau = c.tau;
-  if (c.flags & ~(uint32_t)GEM_FLAG_FUSED) return false;
+  d.flags = c.flags;
+  if (c.flags & ~(uint32_t)(GEM_FLAG_FUSED | GEM_FLAG_NO_ROTATION | GEM_FLAG_ISOTROPIC)) return false;
   if (c.flags & GEM_FLAG_FUSED) {
     if (c.wave <= 0) {   // auto: keep one wave's splat records, lists and images within ~64 MB of L2
       const double per = (double)d.N * (32 + 8 + 4 * (c.tile == 16 ? 2 : 3)) + (double)c.D * c.D * 4 * 3 +
@@ -478,7 +479,7 @@ gem_status gem_step(gem_ctx *ctx, gem_soa *params, const gem_soa *grad, gem_soa 
               (const float4 *)grad->mean_rho, (const float4 *)grad->log_scale, (const float4 *)grad->quat,
               (float4 *)m->mean_rho, (float4 *)m->log_scale, (float4 *)m->quat, (float4 *)v->mean_rho,
               (float4 *)v->log_scale, (float4 *)v->quat, c.lr_mean, c.lr_log_scale, c.lr_quat, c.lr_density, c.beta1,
-              c.beta2, c.eps, (float)bc1, (float)bc2, s, ctx->launches);
+              c.beta2, c.eps, (float)bc1, (float)bc2, (int)c.flags, s, ctx->launches);
   CK(cudaGetLastError());
   return GEM_OK;
 }

@@ -58,6 +58,7 @@ struct DevStats {      // device-side counters (zeroed per forward)
 
 struct CfgDev {        // resolved config passed by value to kernels
   int D, T, tshift, nt, NT, N, C;   // T = 1 << tshift
+  unsigned flags;                   // gem_config.flags
   float px, k, tau;
   int64_t cap;
 };
@@ -127,7 +128,7 @@ void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho,
 void launch_adam(int N, float4 *p_mr, float4 *p_ls, float4 *p_q, const float4 *g_mr, const float4 *g_ls,
                  const float4 *g_q, float4 *m_mr, float4 *m_ls, float4 *m_q, float4 *v_mr, float4 *v_ls, float4 *v_q,
                  float lr_mean, float lr_ls, float lr_q, float lr_rho, float b1, float b2, float eps, float bc1,
-                 float bc2, cudaStream_t s, int &launches);
+                 float bc2, int flags, cudaStream_t s, int &launches);
 size_t volume_scratch_bytes(int N, int Dv);
 cudaError_t launch_volume(int N, const float4 *mean_rho, const float4 *log_scale, const float4 *quat, int Dv,
                           float vs, float k, float *vol, char *scratch, size_t scratch_bytes, cudaStream_t s,

@@ -12,7 +12,7 @@
 namespace gem {
 namespace {
 
-__global__ void __launch_bounds__(256) k_finalize(int N, const float4 *__restrict__ acc,
+__global__ void __launch_bounds__(256) k_finalize(int N, int no_rot, const float4 *__restrict__ acc,
                                                   const float4 *__restrict__ mr, const float4 *__restrict__ ls,
                                                   const float4 *__restrict__ q, float4 *__restrict__ g_mr,
                                                   float4 *__restrict__ g_ls, float4 *__restrict__ g_q, DevStats *st) {
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) k_finalize(int N, const float4 *__restric
   const float4 gq = make_float4((dw - dot * w) * inv, (dx - dot * x) * inv, (dy - dot * y) * inv, (dz - dot * z) * inv);
   g_mr[j] = make_float4(a0.y, a0.z, a0.w, a0.x);
   g_ls[j] = make_float4(ds[0], ds[1], ds[2], 0.f);
-  g_q[j] = gq;
+  g_q[j] = no_rot ? make_float4(0.f, 0.f, 0.f, 0.f) : gq;   // GEM_FLAG_NO_ROTATION: R fixed to I
   const float chk = a0.x + a0.y + a0.z + a0.w + ds[0] + ds[1] + ds[2] + gq.x + gq.y + gq.z + gq.w;
   if (!isfinite(chk)) st->nonfinite = 1;
 }
@@ -82,6 +82,7 @@ struct AdamArgs {
   const float4 *g[3];
   float4 *m[3], *v[3];
   float lr_mean, lr_ls, lr_q, lr_rho, b1, b2, eps, bc1, bc2;
+  int flags;   // GEM_FLAG_NO_ROTATION / GEM_FLAG_ISOTROPIC
 };
 
 __global__ void __launch_bounds__(256) k_adam(int N, AdamArgs A) {
@@ -98,6 +99,13 @@ __global__ void __launch_bounds__(256) k_adam(int N, AdamArgs A) {
     p.x = adam1(p.x, g.x, m.x, v.x, A.lr_ls, A.b1, A.b2, A.eps, A.bc1, A.bc2);
     p.y = adam1(p.y, g.y, m.y, v.y, A.lr_ls, A.b1, A.b2, A.eps, A.bc1, A.bc2);
     p.z = adam1(p.z, g.z, m.z, v.z, A.lr_ls, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+    if (A.flags & GEM_FLAG_ISOTROPIC) {   // tie the three log-scales to their mean (Table 5)
+      const float mean = (p.x + p.y + p.z) * (1.f / 3.f);
+      p.x = p.y = p.z = mean;
+    }
+  } else if (A.flags & GEM_FLAG_NO_ROTATION) {   // R fixed to the identity (Table 5)
+    p = make_float4(1.f, 0.f, 0.f, 0.f);
+    m = v = make_float4(0.f, 0.f, 0.f, 0.f);
   } else {
     p.x = adam1(p.x, g.x, m.x, v.x, A.lr_q, A.b1, A.b2, A.eps, A.bc1, A.bc2);
     p.y = adam1(p.y, g.y, m.y, v.y, A.lr_q, A.b1, A.b2, A.eps, A.bc1, A.bc2);
@@ -116,15 +124,16 @@ __global__ void __launch_bounds__(256) k_adam(int N, AdamArgs A) {
 void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho, const float4 *log_scale,
                      const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
                      int &launches) {
-  k_finalize<<<(c.N + 255) / 256, 256, 0, s>>>(c.N, acc, mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
+  k_finalize<<<(c.N + 255) / 256, 256, 0, s>>>(c.N, c.flags & GEM_FLAG_NO_ROTATION ? 1 : 0, acc, mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
   ++launches;
 }
 
 void launch_adam(int N, float4 *p_mr, float4 *p_ls, float4 *p_q, const float4 *g_mr, const float4 *g_ls,
                  const float4 *g_q, float4 *m_mr, float4 *m_ls, float4 *m_q, float4 *v_mr, float4 *v_ls, float4 *v_q,
                  float lr_mean, float lr_ls, float lr_q, float lr_rho, float b1, float b2, float eps, float bc1,
-                 float bc2, cudaStream_t s, int &launches) {
+                 float bc2, int flags, cudaStream_t s, int &launches) {
   AdamArgs A;
+  A.flags = flags;
   A.p[0] = p_mr; A.p[1] = p_ls; A.p[2] = p_q;
   A.g[0] = g_mr; A.g[1] = g_ls; A.g[2] = g_q;
   A.m[0] = m_mr; A.m[1] = m_ls; A.m[2] = m_q;

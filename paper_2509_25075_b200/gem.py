@@ -34,11 +34,22 @@ class GemConfig:
     eps: float = 1e-8
     fused: bool = False   # L2-resident wave pipeline (GEM_FLAG_FUSED)
     wave: int = 0         # particles per wave (0 = auto)
+    ablation: str = "full"   # Table 5: full | no_rotation | isotropic_scale | both
 
     def c(self) -> _b.GemConfigC:
         return _b.GemConfigC(self.D, self.pixel_size, self.n_gauss, self.max_batch, self.cull_k, self.tau, self.tile,
                              self.list_capacity, self.lr_mean, self.lr_log_scale, self.lr_quat, self.lr_density,
-                             self.beta1, self.beta2, self.eps, _b.GEM_FLAG_FUSED if self.fused else 0, self.wave)
+                             self.beta1, self.beta2, self.eps, self.flags(), self.wave)
+
+    def flags(self) -> int:
+        if self.ablation not in ("full", "no_rotation", "isotropic_scale", "both"):
+            raise ValueError(f"unknown ablation {self.ablation!r}")
+        f = _b.GEM_FLAG_FUSED if self.fused else 0
+        if self.ablation in ("no_rotation", "both"):
+            f |= _b.GEM_FLAG_NO_ROTATION
+        if self.ablation in ("isotropic_scale", "both"):
+            f |= _b.GEM_FLAG_ISOTROPIC
+        return f
 
 
 class SoA:

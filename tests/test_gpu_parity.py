@@ -348,3 +348,39 @@ def test_R_config_bench_batch_sampled(gem, orc):
     tot = sum(parts)
     for name, cols in CLASSES.items():
         assert maxnorm_rel(g["grad"][:, cols], tot[:, cols]) < 1e-5, name
+
+
+@pytest.mark.parametrize("ablation", ["no_rotation", "isotropic_scale", "both"])
+def test_ablation_flags(gem, orc, ablation):
+    """Table 5 ablations: no_rotation keeps q = (1,0,0,0) with an exactly zero
+    quaternion gradient; isotropic_scale leaves the three log-scales of every Gaussian equal after
+    every step.  The other gradient classes are the unablated ones (oracle)."""
+    case = make_case("T", B=3, seed=14)
+    w = case["w"]
+    dev = torch.device("cuda", 0)
+    mr, ls, q = (a.copy() for a in case["params"])
+    if ablation in ("no_rotation", "both"):
+        q[:] = [1.0, 0.0, 0.0, 0.0]
+    if ablation in ("isotropic_scale", "both"):
+        ls[:, :3] = ls[:, :3].mean(axis=1, keepdims=True)
+    case = dict(case, params=(mr, ls, q))
+    cfg = gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=3, ablation=ablation)
+    tr = gem.Trainer(cfg, gem.SoA.from_arrays(mr, ls, q, dev), dev)
+    t = lambda a: torch.from_numpy(a).to(dev)
+    tr.step_ctx.forward(tr.params, t(case["rot"]), t(case["shift"]), t(case["ctf"]), t(case["obs"]))
+    tr.step_ctx.backward(tr.params, tr.grad)
+    g = tr.grad.t.permute(1, 0, 2).reshape(w.N, 12).cpu().numpy()
+    o = oracle_out(orc, case, want=())
+    for name, cols in CLASSES.items():
+        if name == "q" and ablation in ("no_rotation", "both"):
+            assert np.all(g[:, 8:12] == 0.0)
+        else:
+            assert maxnorm_rel(g[:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+    for k in range(3):
+        tr.train_step(t(case["rot"]), t(case["shift"]), t(case["ctf"]), t(case["obs"]))
+        p = tr.params.t.cpu().numpy()
+        if ablation in ("no_rotation", "both"):
+            assert np.all(p[2] == np.array([1, 0, 0, 0], np.float32))
+        if ablation in ("isotropic_scale", "both"):
+            assert np.all(p[1][:, 0] == p[1][:, 1]) and np.all(p[1][:, 1] == p[1][:, 2])
+        assert np.isfinite(p).all()
