@@ -47,6 +47,10 @@ CONFIGS = {
     "R": Workload("R", 50_000, 256, 1.31, 105_000),
     "P": Workload("P", 100_000, 256, 1.31, 130_000),
     "X": Workload("X", 500_000, 384, 1.0, 1_000_000),
+    # desk-scale round trip (SPEC acceptance 3): M = 2000 model Gaussians, d = 64,
+    # 1.5 A pixels, n = 2000 particles; ground truth = a 200-Gaussian phantom ("A_gt")
+    "A": Workload("A", 2_000, 64, 1.5, 2_000),
+    "A_gt": Workload("A_gt", 200, 64, 1.5, 2_000),
 }
 
 

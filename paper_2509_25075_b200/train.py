@@ -7,9 +7,12 @@
   in a small versioned binary format; save -> load -> save is byte-identical and, since the GPU
   step is bitwise deterministic, resuming reproduces the uninterrupted run bit for bit.
 * ``split_halves``: the gold-standard half split.
-* ``fsc`` / ``resolution``: Fourier shell correlation of two half-map volumes and the 0.143
-  criterion (Eq. 9).  An evaluation metric, not part of the training step: computed on
-  the host with numpy.
+* ``fsc`` / ``resolution`` / ``gsfsc``: Fourier shell correlation of two half-map volumes and
+  the 0.143 criterion (Eq. 9).  An evaluation metric, not part of the training step:
+  computed on the host with numpy.
+* ``simulate`` / ``train_halves``: the synthetic round trip (SPEC acceptance 3) -- images
+  of a ground-truth Gaussian set through libgem's forward + CTF plus noise, then two independent
+  half-set reconstructions whose volumes (gem_render_volume) give the GSFSC.
 """
 from __future__ import annotations
 
@@ -127,12 +130,115 @@ def fsc(vol_a, vol_b):
 
 
 def resolution(curve, D: int, voxel_size: float, threshold: float = 0.143) -> float:
-    """Resolution (Angstrom) at the first shell s >= 1 where the FSC falls below ``threshold``:
-    D * voxel_size / s; returns 2 * voxel_size (Nyquist) if it never does."""
-    for s in range(1, len(curve)):
-        if curve[s] < threshold:
-            return D * voxel_size / s
+    """Resolution (Angstrom) where the FSC first drops below ``threshold`` (Fig. 4 caption,
+    P:335-347): walking shells s >= 1 from low to high frequency, the crossing between shell s-1
+    (>= threshold) and shell s (< threshold) is linearly interpolated to the shell coordinate
+    s* = s-1 + (c[s-1] - threshold) / (c[s-1] - c[s]) and reported as D * voxel_size / s*
+    (shell s has frequency s / (D voxel_size)).  No crossing -> 2 * voxel_size (Nyquist); a curve
+    already below threshold at shell 1 reports D * voxel_size (the box)."""
+    c = np.asarray(curve, dtype=np.float64)
+    for s in range(1, len(c)):
+        if c[s] < threshold:
+            if s == 1 and c[0] < threshold:
+                return float(D * voxel_size)
+            lo = c[s - 1]
+            frac = (lo - threshold) / (lo - c[s]) if lo > c[s] else 0.0
+            sstar = (s - 1) + min(max(frac, 0.0), 1.0)
+            return float(D * voxel_size / max(sstar, 1.0))
     return 2.0 * voxel_size
+
+
+def gsfsc(vol_a, vol_b, voxel_size: float, threshold: float = 0.143):
+    """Gold-standard FSC of two half-map volumes: (curve, resolution at ``threshold``)."""
+    c = fsc(vol_a, vol_b)
+    return c, resolution(c, np.asarray(vol_a).shape[0], voxel_size, threshold)
+
+
+def simulate(phantom, data: dict, D: int, pixel_size: float, snr: float, seed: int, batch: int = 64):
+    """Observed images of a ground-truth Gaussian set ``phantom`` (gem.SoA) for the poses/CTFs in
+    ``data`` (rot, shift, ctf device tensors): the GEM forward through the CTF (wide cull, k = 5)
+    plus white noise with per-image variance var(clean) / snr.  Fills data['obs']."""
+    import torch
+    from . import gem
+    n = data["rot"].shape[0]
+    dev = data["rot"].device
+    gen = gem.GemStep(gem.GemConfig(D=D, pixel_size=pixel_size, n_gauss=phantom.N, max_batch=batch,
+                                    cull_k=5.0), dev)
+    obs = torch.empty(n, D, D, device=dev)
+    zeros = torch.zeros(batch, D, D, device=dev)
+    g = torch.Generator(device=dev).manual_seed(seed)
+    for s0 in range(0, n, batch):
+        sl = slice(s0, min(n, s0 + batch))
+        b = sl.stop - sl.start
+        gen.forward(phantom, data["rot"][sl], data["shift"][sl], data["ctf"][sl], zeros[:b], pred=obs[sl])
+        clean = obs[sl]
+        sd = clean.std(dim=(1, 2), keepdim=True) / snr ** 0.5
+        obs[sl] = clean + sd * torch.randn(clean.shape, device=dev, generator=g)
+    torch.cuda.current_stream(dev).synchronize()
+    gen.close()
+    data["obs"] = obs
+    return data
+
+
+def train_halves(make_trainer, data: dict, epochs: int, batch: int, seed: int):
+    """Gold-standard training: split the particles in two seeded halves
+    and train an independent model on each (derived seeds).  ``make_trainer(h)`` returns a fresh
+    gem.Trainer for half h in {0, 1}; its initial state should come from a seed derived from h
+    too, so the halves share nothing (a shared random init correlates the halves' high
+    frequencies and inflates the GSFSC).  Returns (trainer_a, trainer_b, history_a, history_b)."""
+    import torch
+    n = data["rot"].shape[0]
+    out = []
+    for h, idx in enumerate(split_halves(n, seed)):
+        sel = torch.as_tensor(idx, device=data["rot"].device)
+        half = {k: v.index_select(0, sel) for k, v in data.items()}
+        tr = make_trainer(h)
+        out.append((tr, fit(tr, half, epochs, batch, seed=seed * 2 + 1 + h)))
+    return out[0][0], out[1][0], out[0][1], out[1][1]
+
+
+def roundtrip(n: int = 2000, epochs: int = 30, batch: int = 64, snr: float = 0.5, seed: int = 0,
+              ablations=("full", "no_rotation", "isotropic_scale", "both"), lr_scale: float = 1.0,
+              device=None):
+    """SPEC acceptance 3/4 on config A: simulate ``n`` images of the 200-Gaussian
+    ground truth (A_gt) at d = 64, 1.5 A, ``snr``; for each ablation train two independent
+    half-set models of 2000 Gaussians from SPEC random_init (one init seed per half) for
+    ``epochs``; render both half volumes (gem_render_volume, d^3 at the pixel size) and report
+    the GSFSC resolution at 0.143 and FSC(mean of halves, ground truth) at 0.5, in Angstrom."""
+    import time
+    import torch
+    from . import gem, synth
+    dev = device or torch.device("cuda", 0)
+    w, wg = synth.CONFIGS["A"], synth.CONFIGS["A_gt"]
+    px = float(np.float32(w.px))
+    gt = gem.SoA.from_arrays(*synth.f32(*synth.phantom(wg, synth.seed_for("A_gt", "phantom", seed))),
+                             device=dev)
+    rot, shift, ctf = synth.f32(*synth.particles(w, n, seed))
+    data = {k: torch.from_numpy(a).to(dev) for k, a in (("rot", rot), ("shift", shift), ("ctf", ctf))}
+    simulate(gt, data, w.D, px, snr, seed=1000 + seed)
+    vctx = gem.GemStep(gem.GemConfig(D=w.D, pixel_size=px, n_gauss=w.N, max_batch=1), dev)
+    gctx = gem.GemStep(gem.GemConfig(D=w.D, pixel_size=px, n_gauss=wg.N, max_batch=1), dev)
+    vol_gt = gctx.render_volume(gt, w.D, px).cpu().numpy()
+    out = {}
+    for abl in ablations:
+        def make(h):
+            cfg = gem.GemConfig(D=w.D, pixel_size=px, n_gauss=w.N, max_batch=batch, ablation=abl,
+                                lr_mean=1e-3 * w.ball_radius * lr_scale)
+            P0 = synth.f32(*synth.init_model(w, 2 * seed + h))
+            return gem.Trainer(cfg, gem.SoA.from_arrays(*P0, device=dev), dev)
+        t0 = time.time()
+        a, b, ha, hb = train_halves(make, data, epochs, batch, seed)
+        torch.cuda.synchronize(dev)
+        dt = time.time() - t0
+        va = vctx.render_volume(a.params, w.D, px).cpu().numpy()
+        vb = vctx.render_volume(b.params, w.D, px).cpu().numpy()
+        curve, res = gsfsc(va, vb, px)
+        out[abl] = {"gsfsc_A": res, "fsc_gt_0.5_A": resolution(fsc(0.5 * (va + vb), vol_gt), w.D, px, 0.5),
+                    "loss_first": [ha[0], hb[0]], "loss_last": [ha[-1], hb[-1]], "train_s": dt,
+                    "steps": 2 * epochs * -(-(n // 2) // batch), "gsfsc_curve": [float(x) for x in curve]}
+        a.step_ctx.close(); b.step_ctx.close()
+    vctx.close(); gctx.close()
+    return out
 
 
 def _np(a):

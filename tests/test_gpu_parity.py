@@ -279,6 +279,12 @@ def test_workspace_has_no_cubic_term(gem):
         return L.gem_workspace_bytes(ctypes.byref(c))
     r = ws(256) / ws(128)
     assert r < 4.6, r    # quadratic at most (plus lists); D^3 would give 8
+    # SPEC acceptance 6: at M = 50 000 and d = 128 -> 256 the step's whole device footprint
+    # (workspace + params/grad/m/v + batch inputs) grows by <= 1.3x; a dense d^3 path grows 8x
+    def total(D, N=50000, B=8):
+        return ws(D, N, B) + 4 * 48 * N + B * (19 + D * D) * 4
+    r2 = total(256) / total(128)
+    assert r2 <= 1.3, r2
 
 
 def test_host_pipeline_matches_device_steps(gem):

@@ -44,6 +44,27 @@ def test_fsc_identical_independent_and_scaled():
     assert 24 * 2.0 / 10 <= res <= 24 * 2.0 / 3
 
 
+def test_resolution_interpolation_and_gsfsc_examples():
+    """SPEC resolution_at_threshold / gsfsc examples."""
+    D, vox = 32, 1.5
+    # 1.0 up to shell 7, 0.0 from shell 8: the crossing lies (1 - 0.143) of a shell past 7
+    c = np.array([1.0] * 8 + [0.0] * 9)
+    assert math.isclose(T.resolution(c, D, vox), D * vox / (7 + (1 - 0.143)), rel_tol=1e-12)
+    assert T.resolution(np.ones(17), D, vox) == 2 * vox                  # no crossing: Nyquist
+    assert T.resolution(np.zeros(17), D, vox) == D * vox                 # below from the start
+    # monotone in the threshold
+    cc = np.linspace(1.0, -0.2, 17)
+    rs = [T.resolution(cc, D, vox, t) for t in (0.9, 0.5, 0.143)]
+    assert rs[0] >= rs[1] >= rs[2]
+    rng = np.random.default_rng(1)
+    v = rng.standard_normal((D, D, D))
+    assert T.gsfsc(v, v, vox)[1] == 2 * vox
+    # phase-randomised copy: same amplitudes, independent phases -> worse than 8 x voxel
+    ph = np.angle(np.fft.fftn(rng.standard_normal((D, D, D))))
+    w = np.fft.ifftn(np.abs(np.fft.fftn(v)) * np.exp(1j * ph)).real
+    assert T.gsfsc(v, w, vox)[1] > 8 * vox
+
+
 def test_checkpoint_roundtrip_and_errors(tmp_path):
     rng = np.random.default_rng(1)
     p, m, v = (rng.standard_normal((3, 17, 4)).astype(np.float32) for _ in range(3))
@@ -96,3 +117,26 @@ def test_fit_deterministic_and_resume_bitwise(tmp_path):
     T.fit(d, data, epochs=3, batch=B, seed=9, start_epoch=ep)
     assert np.array_equal(d.params.t.cpu().numpy(), a.params.t.cpu().numpy())
     assert np.array_equal(d.m.t.cpu().numpy(), a.m.t.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_roundtrip_acceptance_and_ablation_direction():
+    """SPEC acceptance 3: n = 2000, d = 64, 1.5 A, SNR 0.5, M = 2000, 30 epochs, halves:
+    GSFSC resolution <= 6.0 A and FSC(reconstruction, ground truth) at 0.5 <= 7.5 A.
+    Acceptance 4 / Table 5 direction: every ablation ends at a higher loss
+    than the full model on both halves, and the resolution ordering full <= no_rotation <= both,
+    full <= isotropic <= both holds with 5% slack between adjacent tiers."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = T.roundtrip(seed=0)
+    f = r["full"]
+    assert f["gsfsc_A"] <= 6.0 and f["fsc_gt_0.5_A"] <= 7.5
+    for k in ("no_rotation", "isotropic_scale", "both"):
+        for h in range(2):
+            assert r[k]["loss_last"][h] > f["loss_last"][h], k
+            assert r[k]["loss_last"][h] < r[k]["loss_first"][h], k
+    res = {k: v["gsfsc_A"] for k, v in r.items()}
+    for lo, hi in (("full", "no_rotation"), ("no_rotation", "both"), ("full", "isotropic_scale"),
+                   ("isotropic_scale", "both")):
+        assert res[lo] <= 1.05 * res[hi], (lo, hi, res)
