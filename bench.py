@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--ring", type=int, default=1024, help="distinct device-resident particles per GPU")
     ap.add_argument("--fused", action="store_true", help="L2-resident wave pipeline (GEM_FLAG_FUSED)")
     ap.add_argument("--wave", type=int, default=0, help="particles per wave (0 = auto)")
+    ap.add_argument("--zsort", action="store_true", help="P:227 z-sorted tile lists (GEM_FLAG_ZSORT)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kernel-events", action="store_true",
@@ -223,7 +224,7 @@ def main():
     params = gem.SoA.from_arrays(mr, ls, q, dev)
     phantom = gem.SoA.from_arrays(*synth.f32(*synth.phantom(w, synth.seed_for(w.name, "phantom", 0))), dev)
     cfg = gem.GemConfig(D=w.D, pixel_size=px, n_gauss=w.N, max_batch=B, tile=args.tile,
-                        lr_mean=1e-3 * w.ball_radius, fused=args.fused, wave=args.wave)
+                        lr_mean=1e-3 * w.ball_radius, fused=args.fused, wave=args.wave, zsort=args.zsort)
 
     # device-resident ring of distinct synthetic particles (per-rank seeds)
     rot_np, sh_np, ctf_np = synth.f32(*synth.particles(w, ring, 1000 + rank))
@@ -369,7 +370,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{w.name}: EMPIAR-10028-shaped, N={w.N} Gaussians, D={w.D}, px={w.px} A",
                    "model_state": args.state, "batch_per_gpu": B, "global_batch": B * world, "tile": args.tile,
-                   "fused_waves": args.fused, "wave": int(st["wave"]),
+                   "fused_waves": args.fused, "wave": int(st["wave"]), "zsort": args.zsort,
                    "ring_particles_per_gpu": ring, "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2: per-step working set (splat records "
                          f"{B * w.N * 32 / 1e6:.0f} MB + images) and a {ring}-particle ring "

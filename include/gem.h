@@ -97,8 +97,14 @@ typedef struct {
  * GEM_FLAG_NO_ROTATION  "No Rotation, fix R_i = I": gem_step writes q = (1, 0, 0, 0) and the
  *                       quaternion gradient from gem_backward is exactly zero.
  * GEM_FLAG_ISOTROPIC    "Isotropic Scaling": after every gem_step the three log-scales of each
- *                       Gaussian are set to their mean (S:361 reading). */
-enum { GEM_FLAG_FUSED = 1, GEM_FLAG_NO_ROTATION = 2, GEM_FLAG_ISOTROPIC = 4 };
+ *                       Gaussian are set to their mean (S:361 reading).
+ * Paper-faithful selection order ("sort the selected Gaussians along the z-axis and
+ * accumulate them starting from the lowest z value"):
+ * GEM_FLAG_ZSORT        every (particle, tile) list is ordered by (z_ij, j) ascending, z_ij the
+ *                       camera-frame depth of Gaussian j's centre, ((W20 mx + W21 my) + W22 mz)
+ *                       in fp64 without FMA (W = P_i^T); gem_export_lists returns that order.
+ *                       Costs one sort kernel and a list-sized scratch buffer in the workspace. */
+enum { GEM_FLAG_FUSED = 1, GEM_FLAG_NO_ROTATION = 2, GEM_FLAG_ISOTROPIC = 4, GEM_FLAG_ZSORT = 8 };
 
 /* Gaussian parameter store (a0): three float4 arrays of length N.
  *   mean_rho [N] = (mu_x, mu_y, mu_z [Angstrom], rho)

@@ -128,6 +128,23 @@ def lists(aabb, visible, D, T):
     return tile_off, base, ids[:tot].copy()
 
 
+# -------------------------------------------------------------------- O4z
+def zsort_lists(tile_off, base, ids, splat):
+    """O4z: "we sort the selected Gaussians along the z-axis and accumulate them starting
+    from the lowest z value".  Each tile list of O4 reordered by the key (z_ij, j) ascending,
+    z_ij = splat[i, j, 2] = ((W20 mx + W21 my) + W22 mz) (O2, fp64, no contraction); the id breaks
+    exact ties (reading L24).  Same layout as ``lists``; a library sort serves as the step."""
+    out = ids.copy()
+    B, NT1 = tile_off.shape
+    for i in range(B):
+        z = splat[i, :, 2]
+        for t in range(NT1 - 1):
+            a, b = base[i] + tile_off[i, t], base[i] + tile_off[i, t + 1]
+            seg = ids[a:b]
+            out[a:b] = seg[np.lexsort((seg, z[seg]))]
+    return out
+
+
 # --------------------------------------------------------------------- O5
 def project(params, rot, shift, D, px, k=3.0, tau=0.0, masked=True):
     mr, ls, qu = (_f64(p) for p in params)

@@ -18,6 +18,7 @@ GEM_MEM_DEVICE, GEM_MEM_HOST = 0, 1
 GEM_FLAG_FUSED = 1
 GEM_FLAG_NO_ROTATION = 2   # Table 5 ablation: R fixed to I
 GEM_FLAG_ISOTROPIC = 4     # Table 5 ablation: tied log-scales
+GEM_FLAG_ZSORT = 8         # P:227 z-sorted per-tile lists
 
 
 class GemConfigC(ctypes.Structure):

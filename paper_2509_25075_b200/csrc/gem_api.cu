@@ -37,7 +37,7 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   d.k = c.cull_k;
   d.tau = c.tau;
   d.flags = c.flags;
-  if (c.flags & ~(uint32_t)(GEM_FLAG_FUSED | GEM_FLAG_NO_ROTATION | GEM_FLAG_ISOTROPIC)) return false;
+  if (c.flags & ~(uint32_t)(GEM_FLAG_FUSED | GEM_FLAG_NO_ROTATION | GEM_FLAG_ISOTROPIC | GEM_FLAG_ZSORT)) return false;
   if (c.flags & GEM_FLAG_FUSED) {
     if (c.wave <= 0) {   // auto: keep one wave's splat records, lists and images within ~64 MB of L2
       const double per = (double)d.N * (32 + 8 + 4 * (c.tile == 16 ? 2 : 3)) + (double)c.D * c.D * 4 * 3 +
@@ -105,6 +105,9 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.stage_loss = take(sizeof(double) * (Bm + 1));
   L.cufft_work = take(cufft_bytes);
   L.cufft_work2 = take(cufft_bytes);
+  L.zs_tmp = take((c.flags & GEM_FLAG_ZSORT) ? sizeof(int) * (size_t)L.list_cap : 0);   // z-sort merge scratch
+  L.zs_key = take((c.flags & GEM_FLAG_ZSORT) ? sizeof(uint2) * (size_t)L.list_cap : 0);  // (id, fp32 depth key)
+  L.zs_queue = take((c.flags & GEM_FLAG_ZSORT) ? sizeof(int4) * (W * d.NT + 1) : 0);     // segment queue
   L.total = o;
   return L;
 }
@@ -171,7 +174,7 @@ gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r, cuf
 }
 
 const char *kProfNames[P_COUNT] = {"prep", "splat_count", "scan", "fill", "render_fwd", "fft_r2c",
-                                   "ctf_loss", "fft_c2r", "fft_r2c_obs", "render_bwd", "bwd_reduce", "finalize", "adam", "volume"};
+                                   "ctf_loss", "fft_c2r", "fft_r2c_obs", "render_bwd", "bwd_reduce", "finalize", "adam", "volume", "zsort"};
 
 struct Prof {
   gem_ctx *ctx;
@@ -395,7 +398,13 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
                          ctx->launches); }
     const int64_t nh = (int64_t)nb * c.NT * c.C;
     { Prof p(ctx, s, P_SCAN); launch_scan(hist, base, nh, at<int>(ctx, L.scan_blk), (nh + 4095) / 4096, st, c.cap, s, ctx->launches); }
-    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<int>(ctx, L.subcnt), ids, s, ctx->launches); }
+    uint2 *zpair = (c.flags & GEM_FLAG_ZSORT) ? at<uint2>(ctx, L.zs_key) : nullptr;
+    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<int>(ctx, L.subcnt), ids, (const float4 *)params->mean_rho, rw, zpair, s, ctx->launches); }
+    if (zpair) {
+      Prof p(ctx, s, P_ZSORT);
+      launch_zsort(c, nb, base, (const float4 *)params->mean_rho, rw, ids, zpair, at<int>(ctx, L.zs_tmp),
+                   at<int>(ctx, L.zs_queue), s, ctx->launches);
+    }
     float *proj = proj_out ? proj_out + p0 * DD : at<float>(ctx, L.proj);
     { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, base, ids, proj, at<int>(ctx, L.ticket), s, ctx->launches); }
     CKF(cufftSetStream(r2c, s));

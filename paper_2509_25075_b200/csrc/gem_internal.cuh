@@ -39,7 +39,7 @@ struct __align__(16) SplatRec {
 
 struct Layout {  // byte offsets into the caller's workspace
   size_t prep, rec, box, hist, subcnt, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slot_a, slot_b, acc, loss_part, ctf_par,
-      stats, ticket, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, cufft_work2, total;
+      stats, ticket, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, cufft_work2, zs_tmp, zs_key, zs_queue, total;
   int64_t n_hist;       // B_max * NT * C
   int64_t n_scan_blk;
   int64_t list_cap;
@@ -95,8 +95,22 @@ struct gem_ctx {
 
 namespace gem {
 enum ProfKind { P_PREP, P_SPLAT, P_SCAN, P_FILL, P_RENDER_FWD, P_FFT_R2C, P_CTF_LOSS, P_FFT_C2R, P_FFT_OBS, P_RENDER_BWD,
-                P_BWD_REDUCE, P_FINALIZE, P_ADAM, P_VOLUME, P_COUNT };
+                P_BWD_REDUCE, P_FINALIZE, P_ADAM, P_VOLUME, P_ZSORT, P_COUNT };
 }
+
+// ---------------------------------------------------------------- z-sort keys (GEM_FLAG_ZSORT)
+namespace gem {
+// camera-frame depth of Gaussian j under pose i, ((W20 mx + W21 my) + W22 mz), W = P^T, in fp64
+// without contraction (w0, w1, w2 = P[2], P[5], P[8]); the z-sort key (L24)
+__device__ __forceinline__ double zdepth64(float4 m, double w0, double w1, double w2) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(w0, (double)m.x), __dmul_rn(w1, (double)m.y)), __dmul_rn(w2, (double)m.z));
+}
+// order-preserving map of an fp32 value to uint32
+__device__ __forceinline__ unsigned ord32(float z) {
+  const unsigned b = __float_as_uint(z);
+  return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+}  // namespace gem
 
 // ---------------------------------------------------------------- kernels
 namespace gem {
@@ -107,8 +121,11 @@ void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const flo
                         cudaStream_t s, int &launches);
 void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, DevStats *st, int64_t cap, cudaStream_t s,
                  int &launches);
-void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids, cudaStream_t s,
+void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,
+                 const float4 *mean_rho, const float *rot, uint2 *zpair, cudaStream_t s,
                  int &launches);
+void launch_zsort(const CfgDev &c, int B, const int *base, const float4 *mean_rho, const float *rot, int *ids,
+                  const uint2 *zpair, int *tmp, int *queue, cudaStream_t s, int &launches);
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
                        int *ticket, cudaStream_t s, int &launches);
 void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, void *ctf_par, float2 *spec_hat, const float2 *spec_obs,

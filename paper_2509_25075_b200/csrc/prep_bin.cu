@@ -366,9 +366,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int *__restrict__ out
 // per-tile sets equal the oracle's (reading L9: only the set and its determinism matter).
 
 
+// ZK (GEM_FLAG_ZSORT): entries are written as (id, z-sort key ord32(fp32(z_ij))) pairs to
+// zpair[slot] instead of ids[slot] -- one 8-byte store costs the same DRAM sectors as the 4-byte
+// id -- with the key computed once per Gaussian from a coalesced read of mean_rho; the sort
+// kernel reads the pairs and writes the sorted ids.
+template <bool ZK>
 __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 *__restrict__ box,
                                                           const int *__restrict__ base,
-                                                          const int *__restrict__ subcnt, int *__restrict__ ids) {
+                                                          const int *__restrict__ subcnt, int *__restrict__ ids,
+                                                          const float4 *__restrict__ mean_rho,
+                                                          const float *__restrict__ rot, uint2 *__restrict__ zpair) {
   extern __shared__ int cnt[];   // [kFillWarps][NT] cursors
   const int i = blockIdx.y, ch = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int *mine = cnt + w * c.NT;
@@ -387,6 +394,8 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
   }
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
+  double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+  if (ZK) { w0 = (double)rot[9 * i + 2]; w1 = (double)rot[9 * i + 5]; w2 = (double)rot[9 * i + 8]; }
   for (int step = 0; step < kSub / 32; ++step) {     // pass 2: deterministic fill
     const int j0 = jsub + step * 32;
     if (j0 >= c.N) break;
@@ -400,6 +409,8 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
         ntu = (uhi >> c.tshift) - tu0 + 1; ntv = (vhi >> c.tshift) - tv0 + 1;
       }
     }
+    unsigned key = 0;
+    if (ZK && ntu > 0) key = ord32(__double2float_rn(zdepth64(__ldg(mean_rho + j), w0, w1, w2)));
     // slot-major order: every lane's tile (dv, du) of its rectangle, (dv, du) ascending, then lane
     const int mu = __reduce_max_sync(0xffffffffu, (unsigned)max(ntu, 0));
     const int mv = __reduce_max_sync(0xffffffffu, (unsigned)ntv);
@@ -411,7 +422,10 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
         const int rank = __popc(m & lt);
         if (active) {
           const int slot = mine[t] + rank;
-          if ((int64_t)slot < c.cap) ids[slot] = j;
+          if ((int64_t)slot < c.cap) {
+            if (ZK) zpair[slot] = make_uint2((unsigned)j, key);
+            else ids[slot] = j;
+          }
         }
         __syncwarp();
         if (active && rank == 0) mine[t] += __popc(m);
@@ -451,12 +465,18 @@ void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, Dev
   launches += 3;
 }
 
-void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids, cudaStream_t s,
-                 int &launches) {
+void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,
+                 const float4 *mean_rho, const float *rot, uint2 *zpair, cudaStream_t s, int &launches) {
   dim3 grid(c.C, B);
   const size_t smem = (size_t)kFillWarps * c.NT * sizeof(int);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_fill<<<grid, kFillWarps * 32, smem, s>>>(c, box, base, subcnt, ids);
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(k_fill<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_fill<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  if (zpair)
+    k_fill<true><<<grid, kFillWarps * 32, smem, s>>>(c, box, base, subcnt, ids, mean_rho, rot, zpair);
+  else
+    k_fill<false><<<grid, kFillWarps * 32, smem, s>>>(c, box, base, subcnt, ids, mean_rho, rot, zpair);
   ++launches;
 }
 

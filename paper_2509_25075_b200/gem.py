@@ -35,6 +35,7 @@ class GemConfig:
     fused: bool = False   # L2-resident wave pipeline (GEM_FLAG_FUSED)
     wave: int = 0         # particles per wave (0 = auto)
     ablation: str = "full"   # Table 5: full | no_rotation | isotropic_scale | both
+    zsort: bool = False      # P:227 z-sorted per-tile lists (GEM_FLAG_ZSORT)
 
     def c(self) -> _b.GemConfigC:
         return _b.GemConfigC(self.D, self.pixel_size, self.n_gauss, self.max_batch, self.cull_k, self.tau, self.tile,
@@ -45,6 +46,8 @@ class GemConfig:
         if self.ablation not in ("full", "no_rotation", "isotropic_scale", "both"):
             raise ValueError(f"unknown ablation {self.ablation!r}")
         f = _b.GEM_FLAG_FUSED if self.fused else 0
+        if self.zsort:
+            f |= _b.GEM_FLAG_ZSORT
         if self.ablation in ("no_rotation", "both"):
             f |= _b.GEM_FLAG_NO_ROTATION
         if self.ablation in ("isotropic_scale", "both"):

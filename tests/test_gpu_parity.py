@@ -42,11 +42,11 @@ def make_case(wname="T", B=4, seed=0, N=None, D=None, state="steady", morton=Tru
     return dict(w=w, params=(mr, ls, q), rot=rot, shift=shift, ctf=ctf, obs=obs, px=float(np.float32(w.px)))
 
 
-def run_gpu(gem, case, tile=16, want_lists=False, cap=0, host=False, fused=False, wave=0):
+def run_gpu(gem, case, tile=16, want_lists=False, cap=0, host=False, fused=False, wave=0, zsort=False):
     w = case["w"]
     B = case["rot"].shape[0]
     cfg = gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=B, tile=tile, list_capacity=cap,
-                        fused=fused, wave=wave)
+                        fused=fused, wave=wave, zsort=zsort)
     st = gem.GemStep(cfg)
     dev = st.device
     P = gem.SoA.from_arrays(*case["params"], device=dev)
@@ -392,3 +392,57 @@ def test_ablation_flags(gem, orc, ablation):
         if ablation in ("isotropic_scale", "both"):
             assert np.all(p[1][:, 0] == p[1][:, 1]) and np.all(p[1][:, 1] == p[1][:, 2])
         assert np.isfinite(p).all()
+
+
+def assert_zsorted_lists_exact(orc, case, lists, tile):
+    """f1: with GEM_FLAG_ZSORT every exported tile list equals the oracle's O4z list
+    element by element -- the (depth, id) order is a bit-exact function of the inputs."""
+    w = case["w"]
+    aabb, vis, sp = orc.splats(case["params"], case["rot"], case["shift"], w.D, case["px"])
+    tile_off, base, ids = orc.lists(aabb, vis, w.D, tile)
+    zs = orc.zsort_lists(tile_off, base, ids, sp)
+    n = 0
+    for i, (g_off, g_ids, _) in enumerate(lists):
+        assert np.array_equal(g_off, tile_off[i]), i
+        assert np.array_equal(g_ids, zs[base[i]: base[i] + tile_off[i, -1]]), i
+        n += len(g_ids)
+    return n
+
+
+@pytest.mark.parametrize("wname,B,tile", [("T", 4, 8), ("T", 3, 16), ("S", 2, 8)])
+def test_zsort_lists_exact_and_parity(gem, orc, wname, B, tile):
+    case = make_case(wname, B=B, seed=21)
+    g = run_gpu(gem, case, tile=tile, want_lists=True, zsort=True)
+    assert assert_zsorted_lists_exact(orc, case, g["lists"], tile) > 0
+    o = oracle_out(orc, case)
+    for i in range(B):
+        assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL, i
+    assert np.all(np.abs(g["loss"][:-1] - o["loss"]) < LOSS_TOL * o["loss"])
+    for name, cols in CLASSES.items():
+        assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+    # deterministic: a second run gives the same lists and bytes
+    g2 = run_gpu(gem, case, tile=tile, want_lists=True, zsort=True)
+    assert np.array_equal(g["proj"], g2["proj"]) and np.array_equal(g["grad"], g2["grad"])
+    assert all(np.array_equal(a[1], b[1]) for a, b in zip(g["lists"], g2["lists"]))
+
+
+def test_zsort_long_segments_merge_path(gem, orc):
+    """Tile lists longer than the 4096-entry shared-memory sort take the run + merge path."""
+    rng = np.random.default_rng(3)
+    N, D, B = 9000, 32, 2
+    w = synth.Workload("Z", N, D, 1.0, B)
+    mu = np.concatenate([rng.uniform(-2.0, 2.0, (N, 2)), rng.uniform(-20.0, 20.0, (N, 1))], 1)
+    mr = np.concatenate([mu, rng.uniform(0.5, 1.5, (N, 1))], 1)
+    ls = np.concatenate([np.log(rng.uniform(1.5, 2.5, (N, 3))), np.zeros((N, 1))], 1)
+    q = rng.standard_normal((N, 4)); q /= np.linalg.norm(q, axis=1, keepdims=True)
+    rot, shift, ctf = synth.particles(w, B, 4)
+    mr, ls, q, rot, shift, ctf = synth.f32(mr, ls, q, rot, np.zeros((B, 2)), ctf)
+    case = dict(w=w, params=(mr, ls, q), rot=rot, shift=shift, ctf=ctf,
+                obs=synth.f32(synth.noise_images(w, B, 4, scale=5.0)), px=1.0)
+    g = run_gpu(gem, case, tile=8, want_lists=True, zsort=True)
+    lens = [np.diff(off).max() for off, _, _ in g["lists"]]
+    assert max(lens) > 4096, lens
+    assert assert_zsorted_lists_exact(orc, case, g["lists"], 8) > 0
+    o = oracle_out(orc, case, want=("proj",))
+    for i in range(B):
+        assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL, i

@@ -280,3 +280,43 @@ def test_lists_brute_force(orc, D, T):
     far = (np.array([[1e4, 0, 0, 1.0]]), np.zeros((1, 4)), np.array([[1.0, 0, 0, 0]]))
     a2, v2, _ = orc.splats(far, rot[:1], sh[:1], D, px)
     assert v2.sum() == 0
+
+
+def test_zsort_lists_depth_order(orc):
+    """O4z: each tile list is the O4 set ordered by camera depth, nearest (lowest z)
+    first, ties by id.  Pinned against a hand-built case (identity pose: z = mu_z, so the order is
+    known without any projection arithmetic) and, on random poses, against depths computed by an
+    independent route (scipy rotation matrix transposed, applied with numpy)."""
+    # hand-built: five Gaussians stacked on the optical axis at known depths, two of them tied
+    mu_z = [3.0, -2.0, 7.5, -2.0, 0.25]
+    mr = np.array([[0.0, 0.0, z, 1.0] for z in mu_z])
+    ls = np.zeros((5, 4))
+    qu = np.tile([1.0, 0, 0, 0], (5, 1))
+    rot = np.eye(3).reshape(1, 9)
+    aabb, vis, sp = orc.splats((mr, ls, qu), rot, np.zeros((1, 2)), 16, 1.0)
+    tile_off, base, ids = orc.lists(aabb, vis, 16, 8)
+    z = orc.zsort_lists(tile_off, base, ids, sp)
+    nt = 2
+    for t in range(nt * nt):
+        seg = z[tile_off[0, t]: tile_off[0, t + 1]]
+        if len(seg):
+            assert list(seg) == [1, 3, 4, 0, 2]      # z = -2 (id 1), -2 (id 3), 0.25, 3, 7.5
+    # random poses: a permutation of the O4 set, nondecreasing in the independent depth
+    rng = np.random.default_rng(5)
+    N, B, D, T, px = 80, 3, 32, 8, 1.0
+    params = _random_case(rng, N, D, px, sig_px=(0.6, 3.0), spread=0.6)
+    R = np.stack([Rotation.random(random_state=70 + s).as_matrix() for s in range(B)])
+    sh = rng.uniform(-3, 3, (B, 2))
+    aabb, vis, sp = orc.splats(params, R.reshape(B, 9), sh, D, px)
+    tile_off, base, ids = orc.lists(aabb, vis, D, T)
+    zs = orc.zsort_lists(tile_off, base, ids, sp)
+    checked = 0
+    for i in range(B):
+        depth = (R[i].T @ params[0][:, :3].T)[2]        # W = P^T, third row
+        for t in range(tile_off.shape[1] - 1):
+            a, b = base[i] + tile_off[i, t], base[i] + tile_off[i, t + 1]
+            assert sorted(zs[a:b]) == list(ids[a:b])
+            d = depth[zs[a:b]]
+            assert np.all(np.diff(d) >= -1e-12)
+            checked += b - a
+    assert checked > 100
