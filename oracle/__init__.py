@@ -66,7 +66,7 @@ def lib():
         _lib.orc_apply_ctf.restype = d
         _lib.orc_apply_ctf.argtypes = [i, p, p, p]
         _lib.orc_loss_grad.restype = d
-        _lib.orc_loss_grad.argtypes = [i, i, p, p, p, p, p, p, p, i, d, d, d, p, p, p, p, p, p, p, p]
+        _lib.orc_loss_grad.argtypes = [i, i, p, p, p, p, p, p, p, i, d, d, d, i, p, p, p, p, p, p, p, p]
         _lib.orc_adam.restype = None
         _lib.orc_adam.argtypes = [i, p, p, p, p, ll, p, d, d, d]
         _lib.orc_volume.restype = None
@@ -146,23 +146,26 @@ def zsort_lists(tile_off, base, ids, splat):
 
 
 # --------------------------------------------------------------------- O5
-def project(params, rot, shift, D, px, k=3.0, tau=0.0, masked=True):
+def project(params, rot, shift, D, px, k=3.0, tau=0.0, masked=True, pixmask=0):
+    """O5.  ``pixmask`` adds the per-pixel selection variants (2 = exact ellipse Q <= k^2,
+    4 = per-pixel tau |G| >= tau) on top of the AABB mask."""
     mr, ls, qu = (_f64(p) for p in params)
     rot, shift = _f64(rot), _f64(shift)
     N, B = mr.shape[0], rot.shape[0]
     img = np.zeros((B, D, D))
     lib().orc_project(N, B, _ptr(mr), _ptr(ls), _ptr(qu), _ptr(rot), _ptr(shift), D, px, k, tau,
-                      int(masked), _ptr(img))
+                      (int(masked) | int(pixmask)) if masked else 0, _ptr(img))
     return img
 
 
-def project_pixels(params, rot1, shift1, D, px, pix, k=3.0, tau=0.0, masked=True):
+def project_pixels(params, rot1, shift1, D, px, pix, k=3.0, tau=0.0, masked=True, pixmask=0):
     """O5 at sampled pixels pix[n] = (u, v) of one particle."""
     mr, ls, qu = (_f64(p) for p in params)
     rot1, shift1, pix = _f64(rot1).reshape(9), _f64(shift1).reshape(2), _i32(pix).reshape(-1, 2)
     out = np.zeros(pix.shape[0])
     lib().orc_project_pixels(mr.shape[0], _ptr(mr), _ptr(ls), _ptr(qu), _ptr(rot1), _ptr(shift1), D, px, k,
-                             tau, int(masked), pix.shape[0], _ptr(pix), _ptr(out))
+                             tau, (int(masked) | int(pixmask)) if masked else 0, pix.shape[0], _ptr(pix),
+                             _ptr(out))
     return out
 
 
@@ -202,10 +205,11 @@ def apply_ctf(Cgrid, img):
 
 
 # ----------------------------------------------------------------- O7-O10
-def loss_grad(params, rot, shift, ctfp, obs, D, px, k=3.0, tau=0.0, frozen=None, want=()):
+def loss_grad(params, rot, shift, ctfp, obs, D, px, k=3.0, tau=0.0, frozen=None, want=(), pixmask=0):
     """Full forward + backward.  Returns dict with 'loss' [B], 'total', 'grad' [N,12]
     and, if requested in ``want``: 'proj', 'pred', 'gimg' [B,D,D], 'acc' [N,10].
-    ``frozen`` = (aabb[B,N,4], visible[B,N]) freezes the masks."""
+    ``frozen`` = (aabb[B,N,4], visible[B,N]) freezes the masks.  ``pixmask`` selects the
+    per-pixel selection variants as in ``project`` (2 exact ellipse, 4 per-pixel tau)."""
     mr, ls, qu = (_f64(p) for p in params)
     rot, shift, ctfp, obs = _f64(rot), _f64(shift), _f64(ctfp), _f64(obs)
     N, B = mr.shape[0], rot.shape[0]
@@ -217,7 +221,7 @@ def loss_grad(params, rot, shift, ctfp, obs, D, px, k=3.0, tau=0.0, frozen=None,
     if frozen is not None:
         fa, fv = _i32(frozen[0]), _i32(frozen[1])
     tot = lib().orc_loss_grad(N, B, _ptr(mr), _ptr(ls), _ptr(qu), _ptr(rot), _ptr(shift), _ptr(ctfp),
-                              _ptr(obs), D, px, k, tau, _ptr(fa), _ptr(fv), _ptr(out["loss"]),
+                              _ptr(obs), D, px, k, tau, int(pixmask), _ptr(fa), _ptr(fv), _ptr(out["loss"]),
                               _ptr(out["proj"]), _ptr(out["pred"]), _ptr(out["gimg"]), _ptr(out["grad"]),
                               _ptr(out["acc"]))
     out["total"] = tot

@@ -215,7 +215,16 @@ long long orc_lists(int N, int B, int D, int T, const int32_t *aabb, const int32
  *   masked:   I(u,v) = sum_{j visible, (u,v) in AABB_ij} amp exp(-Q/2)
  *   unmasked: I(u,v) = sum_{j non-degenerate} amp exp(-Q/2)  (mask == 1)
  * Q = a dx^2 + 2 b dx dy + c dy^2, dx = x - m_x, dy = y - m_y (Angstrom),
- * every Gaussian at every pixel.  img [B][D][D]. */
+ * every Gaussian at every pixel.  img [B][D][D].
+ * Per-pixel selection variants (reading L26), bits of `masked` / `pixmask`:
+ *   2  exact ellipse: the pixel also needs Q <= k^2 (inside the k-sigma ellipse, not only its box);
+ *   4  per-pixel tau (Eq. 8 "G_j > tau" at the pixel): |amp| exp(-Q/2) >= tau. */
+static int pix_keep(const orc_splat_t *s, double Q, int pixmask, double k, double tau) {
+  if ((pixmask & 2) && !(Q <= k * k)) return 0;
+  if ((pixmask & 4) && !(fabs(s->amp) * exp(-0.5 * Q) >= tau)) return 0;
+  return 1;
+}
+
 void orc_project(int N, int B, const double *mean_rho, const double *log_scale, const double *quat,
                  const double *rot, const double *shift, int D, double px, double k, double tau,
                  int masked, double *img) {
@@ -241,6 +250,7 @@ void orc_project(int N, int B, const double *mean_rho, const double *log_scale, 
           if (!use) continue;
           double dx = x - s->mx, dy = y - s->my;
           double Q = s->a * dx * dx + 2.0 * s->b * dx * dy + s->c * dy * dy;
+          if (masked && !pix_keep(s, Q, masked, k, tau)) continue;
           acc += s->amp * exp(-0.5 * Q);
         }
         img[((size_t)i * D + v) * D + u] = acc;
@@ -273,6 +283,7 @@ void orc_project_pixels(int N, const double *mean_rho, const double *log_scale, 
       if (!use) continue;
       double dx = x - s->mx, dy = y - s->my;
       double Q = s->a * dx * dx + 2.0 * s->b * dx * dy + s->c * dy * dy;
+      if (masked && !pix_keep(s, Q, masked, k, tau)) continue;
       acc += s->amp * exp(-0.5 * Q);
     }
     out[n] = acc;
@@ -396,7 +407,7 @@ double orc_apply_ctf(int D, const double *Cgrid, const double *img, double *out)
  * Returns total loss. */
 double orc_loss_grad(int N, int B, const double *mean_rho, const double *log_scale, const double *quat,
                      const double *rot, const double *shift, const double *ctf, const double *obs, int D,
-                     double px, double k, double tau, const int32_t *frozen_aabb,
+                     double px, double k, double tau, int pixmask, const int32_t *frozen_aabb,
                      const int32_t *frozen_vis, double *loss, double *proj_out, double *pred_out,
                      double *gimg_out, double *grad, double *acc_out) {
   size_t DD = (size_t)D * D;
@@ -426,7 +437,9 @@ double orc_loss_grad(int N, int B, const double *mean_rho, const double *log_sca
           const orc_splat_t *s = &sp[(size_t)i * N + j];
           if (!(s->visible && u >= s->ulo && u <= s->uhi && v >= s->vlo && v <= s->vhi)) continue;
           double dx = x - s->mx, dy = y - s->my;
-          a += s->amp * exp(-0.5 * (s->a * dx * dx + 2.0 * s->b * dx * dy + s->c * dy * dy));
+          double Q = s->a * dx * dx + 2.0 * s->b * dx * dy + s->c * dy * dy;
+          if (pixmask && !pix_keep(s, Q, pixmask, k, tau)) continue;
+          a += s->amp * exp(-0.5 * Q);
         }
         proj[((size_t)i * D + v) * D + u] = a;
       }
@@ -465,7 +478,9 @@ double orc_loss_grad(int N, int B, const double *mean_rho, const double *log_sca
           if (!(u >= s->ulo && u <= s->uhi && v >= s->vlo && v <= s->vhi)) continue;
           double x = ((double)u - half) * px, y = ((double)v - half) * px;
           double dx = x - s->mx, dy = y - s->my;
-          double e = exp(-0.5 * (s->a * dx * dx + 2.0 * s->b * dx * dy + s->c * dy * dy));
+          double Q = s->a * dx * dx + 2.0 * s->b * dx * dy + s->c * dy * dy;
+          if (pixmask && !pix_keep(s, Q, pixmask, k, tau)) continue;
+          double e = exp(-0.5 * Q);
           double gg = gim[((size_t)i * D + v) * D + u];
           double h = gg * s->amp * e;
           La += gg * e;

@@ -320,3 +320,40 @@ def test_zsort_lists_depth_order(orc):
             assert np.all(np.diff(d) >= -1e-12)
             checked += b - a
     assert checked > 100
+
+
+def test_pixel_mask_variants_closed_form(orc):
+    """Per-pixel selection variants (reading L26) against closed forms: an
+    isotropic Gaussian of scale sigma projects to amp exp(-r^2 / (2 sigma^2)), amp = rho sqrt(2 pi)
+    sigma; the exact-ellipse mask keeps r^2 <= k^2 sigma^2 and the per-pixel tau mask keeps
+    amp exp(-r^2 / (2 sigma^2)) >= tau.  An anisotropic rotated Gaussian's ellipse mask equals
+    Q <= k^2 with Q from numpy's inverse of the projected covariance."""
+    D, px, sig, rho, k = 32, 1.0, 2.1, 1.3, 3.0   # 9 sigma^2 = 39.69: no pixel on the boundary
+    params = one_gauss([0.0, 0.0, 0.0], [math.log(sig)] * 3, [1.0, 0, 0, 0], rho)
+    rot, sh = np.eye(3).reshape(1, 9), np.zeros((1, 2))
+    u = np.arange(D) - D // 2
+    r2 = (u[None, :] ** 2 + u[:, None] ** 2) * px * px
+    amp = rho * math.sqrt(2 * math.pi) * sig
+    full = amp * np.exp(-r2 / (2 * sig * sig))
+    box = orc.project(params, rot, sh, D, px, k=k)[0]
+    ell = orc.project(params, rot, sh, D, px, k=k, pixmask=2)[0]
+    np.testing.assert_allclose(ell, np.where(r2 <= k * k * sig * sig, full, 0.0), rtol=1e-12, atol=1e-300)
+    assert np.count_nonzero(box) > np.count_nonzero(ell) > 0      # the AABB keeps the corners
+    tau = 0.3 * amp
+    tm = orc.project(params, rot, sh, D, px, k=k, tau=tau, pixmask=4)[0]
+    np.testing.assert_allclose(tm, np.where(full >= tau, full, 0.0), rtol=1e-12, atol=1e-300)
+    # anisotropic, rotated
+    R = Rotation.random(random_state=9).as_matrix()
+    s = [math.log(1.2), math.log(2.5), math.log(0.9)]
+    q = Rotation.random(random_state=10).as_quat()
+    params = one_gauss([1.0, -2.0, 0.5], s, [q[3], q[0], q[1], q[2]], 1.0)
+    img = orc.project(params, R.reshape(1, 9), sh, D, px, k=k, pixmask=2)[0]
+    Sig = sigma_ref([q[3], q[0], q[1], q[2]], s)
+    W = R.T
+    S2 = (W @ Sig @ W.T)[:2, :2]
+    m = (W @ np.array([1.0, -2.0, 0.5]))[:2]
+    X = np.stack(np.meshgrid(u * px, u * px, indexing="xy"), -1) - m   # [v][u][2]
+    Q = np.einsum("vui,ij,vuj->vu", X, np.linalg.inv(S2), X)
+    near = np.abs(Q - k * k) < 1e-9
+    assert not near.any()
+    assert np.array_equal(img != 0, Q <= k * k)

@@ -113,3 +113,30 @@ def test_batch_gradient_is_sum_over_particles(orc):
     b = orc.loss_grad(params, rot[1:], shift[1:], ctf[1:], obs[1:], D, px)
     assert np.abs(a["grad"] + b["grad"] - full["grad"]).max() < 1e-12 * np.abs(full["grad"]).max()
     assert abs(a["total"] + b["total"] - full["total"]) < 1e-12 * full["total"]
+
+
+@pytest.mark.parametrize("pixmask", [2, 4, 6])
+def test_pixel_mask_variants_gradient_vs_fd(orc, pixmask):
+    """SURVEY §8(f1) variants (exact ellipse Q <= k^2, per-pixel tau of Eq. 8): the oracle
+    gradient restricted to the kept pixels equals central finite differences of its own loss
+    (a step of 1e-6 moves no pixel across a mask boundary in these cases)."""
+    params, rot, shift, ctf, obs, D, px = tiny_case(4)
+    aabb, vis, _ = orc.splats(params, rot, shift, D, px)
+    tau = 0.05
+    frozen = (aabb, vis)
+    base = orc.loss_grad(params, rot, shift, ctf, obs, D, px, tau=tau, frozen=frozen, pixmask=pixmask)
+    plain = orc.loss_grad(params, rot, shift, ctf, obs, D, px, tau=tau, frozen=frozen)
+    assert abs(base["total"] - plain["total"]) > 1e-9 * plain["total"]   # the mask changes the result
+    g = base["grad"]
+    fd = np.zeros_like(g)
+    for j in range(g.shape[0]):
+        for c in [0, 1, 2, 3, 4, 5, 6, 8, 9, 10, 11]:
+            h = 1e-5 if c < 3 else 1e-6
+            lp = orc.loss_grad(flat_to_params(params, j, c, h), rot, shift, ctf, obs, D, px, tau=tau,
+                               frozen=frozen, pixmask=pixmask)["total"]
+            lm = orc.loss_grad(flat_to_params(params, j, c, -h), rot, shift, ctf, obs, D, px, tau=tau,
+                               frozen=frozen, pixmask=pixmask)["total"]
+            fd[j, c] = (lp - lm) / (2 * h)
+    for name, cols in CLASSES.items():
+        err = np.abs(fd[:, cols] - g[:, cols]).max() / np.abs(g[:, cols]).max()
+        assert err < 1e-6, (name, err)
