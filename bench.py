@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--fused", action="store_true", help="L2-resident wave pipeline (GEM_FLAG_FUSED)")
     ap.add_argument("--wave", type=int, default=0, help="particles per wave (0 = auto)")
     ap.add_argument("--zsort", action="store_true", help="P:227 z-sorted tile lists (GEM_FLAG_ZSORT)")
+    ap.add_argument("--pixel-mask", default="aabb", choices=["aabb", "ellipse", "tau", "ellipse+tau"],
+                    help="Eq. 8 per-pixel selection variant (GEM_FLAG_ELLIPSE / GEM_FLAG_PIXEL_TAU)")
+    ap.add_argument("--tau", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kernel-events", action="store_true",
@@ -224,7 +227,8 @@ def main():
     params = gem.SoA.from_arrays(mr, ls, q, dev)
     phantom = gem.SoA.from_arrays(*synth.f32(*synth.phantom(w, synth.seed_for(w.name, "phantom", 0))), dev)
     cfg = gem.GemConfig(D=w.D, pixel_size=px, n_gauss=w.N, max_batch=B, tile=args.tile,
-                        lr_mean=1e-3 * w.ball_radius, fused=args.fused, wave=args.wave, zsort=args.zsort)
+                        lr_mean=1e-3 * w.ball_radius, fused=args.fused, wave=args.wave, zsort=args.zsort,
+                        pixel_mask=args.pixel_mask, tau=args.tau)
 
     # device-resident ring of distinct synthetic particles (per-rank seeds)
     rot_np, sh_np, ctf_np = synth.f32(*synth.particles(w, ring, 1000 + rank))
@@ -370,7 +374,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{w.name}: EMPIAR-10028-shaped, N={w.N} Gaussians, D={w.D}, px={w.px} A",
                    "model_state": args.state, "batch_per_gpu": B, "global_batch": B * world, "tile": args.tile,
-                   "fused_waves": args.fused, "wave": int(st["wave"]), "zsort": args.zsort,
+                   "fused_waves": args.fused, "wave": int(st["wave"]), "zsort": args.zsort, "pixel_mask": args.pixel_mask, "tau": args.tau,
                    "ring_particles_per_gpu": ring, "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2: per-step working set (splat records "
                          f"{B * w.N * 32 / 1e6:.0f} MB + images) and a {ring}-particle ring "

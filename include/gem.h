@@ -104,7 +104,14 @@ typedef struct {
  *                       camera-frame depth of Gaussian j's centre, ((W20 mx + W21 my) + W22 mz)
  *                       in fp64 without FMA (W = P_i^T); gem_export_lists returns that order.
  *                       Costs one sort kernel and a list-sized scratch buffer in the workspace. */
-enum { GEM_FLAG_FUSED = 1, GEM_FLAG_NO_ROTATION = 2, GEM_FLAG_ISOTROPIC = 4, GEM_FLAG_ZSORT = 8 };
+/* Per-pixel selection (Eq. 8 "G_j > tau" at each pixel); the pixel
+ * must lie in the AABB (as always) and in addition:
+ * GEM_FLAG_ELLIPSE      inside the k-sigma ellipse, Q <= cull_k^2 (not only its bounding box);
+ * GEM_FLAG_PIXEL_TAU    |amp_ij| exp(-Q/2) >= tau at the pixel.
+ * Both apply to the forward and, with the same masks, to the backward.  The tile lists stay
+ * AABB-based (a superset).  DESIGN.md §3 L26. */
+enum { GEM_FLAG_FUSED = 1, GEM_FLAG_NO_ROTATION = 2, GEM_FLAG_ISOTROPIC = 4, GEM_FLAG_ZSORT = 8,
+       GEM_FLAG_ELLIPSE = 16, GEM_FLAG_PIXEL_TAU = 32 };
 
 /* Gaussian parameter store (a0): three float4 arrays of length N.
  *   mean_rho [N] = (mu_x, mu_y, mu_z [Angstrom], rho)

@@ -37,7 +37,8 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   d.k = c.cull_k;
   d.tau = c.tau;
   d.flags = c.flags;
-  if (c.flags & ~(uint32_t)(GEM_FLAG_FUSED | GEM_FLAG_NO_ROTATION | GEM_FLAG_ISOTROPIC | GEM_FLAG_ZSORT)) return false;
+  if (c.flags & ~(uint32_t)(GEM_FLAG_FUSED | GEM_FLAG_NO_ROTATION | GEM_FLAG_ISOTROPIC | GEM_FLAG_ZSORT |
+                             GEM_FLAG_ELLIPSE | GEM_FLAG_PIXEL_TAU)) return false;
   if (c.flags & GEM_FLAG_FUSED) {
     if (c.wave <= 0) {   // auto: keep one wave's splat records, lists and images within ~64 MB of L2
       const double per = (double)d.N * (32 + 8 + 4 * (c.tile == 16 ? 2 : 3)) + (double)c.D * c.D * 4 * 3 +

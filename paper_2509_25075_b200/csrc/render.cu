@@ -68,10 +68,21 @@ struct FwdSmem {
   float4 eA[kCH];                // (my, nb2, nc, amp)           tile-local pixel units, log2 scale
   float4 eB[kCH];                // (Fx, Gx, D0, S = 2^{2 na})   f(dx0, dy) = Fx + dy (Gx + nc dy)
   float2 eC[kCH];                // (na, bits)  bits = cu0 | cu1 << 8 | cv0 << 16 | cv1 << 24 | slow << 31
+  float thr[kCH];                // MK: per-pixel keep threshold on |amp e|
   unsigned char bin[NP][kCH];    // entry indices per row pair
 };
 
-template <int T>
+// Per-pixel selection variants (reading L26; GEM_FLAG_ELLIPSE / _PIXEL_TAU): a
+// pixel inside the AABB is kept only if Q <= k^2 and/or |amp| e >= tau, i.e. |amp e| >= thr with
+// thr = max(ELLIPSE ? |amp| exp(-k^2/2) : 0, PIXEL_TAU ? tau : 0), tested on the value the
+// recurrence produces (forward) or on e >= thr / |amp| (backward).
+__device__ __forceinline__ float keep_thr(const CfgDev &c, float amp, float eK) {
+  float t = (c.flags & GEM_FLAG_ELLIPSE) ? fabsf(amp) * eK : 0.f;
+  if (c.flags & GEM_FLAG_PIXEL_TAU) t = fmaxf(t, c.tau);
+  return t;
+}
+
+template <int T, bool MK>
 __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, const SplatRec *__restrict__ rec,
                                                                 const int *__restrict__ base,
                                                                 const int *__restrict__ ids,
@@ -79,6 +90,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
   using SM = FwdSmem<T>;
   constexpr int NP = T / 2, NCP = 32 / NP;
   constexpr float nh = -0.5f * kLog2e;
+  const float eK = MK ? ex2(nh * c.k * c.k) : 0.f;
   extern __shared__ __align__(16) unsigned char fwd_dsm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   SM &sm = reinterpret_cast<SM *>(fwd_dsm)[w];
@@ -154,6 +166,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
         sm.eB[qc] = make_float4(Fx, Gx, D0, ex2(2.f * na));
         sm.eC[qc] = make_float2(na, __int_as_float(cu0 | (cu1 << 8) | (cv0 << 16) | (cv1 << 24) |
                                                    (slow ? (int)0x80000000 : 0)));
+        if (MK) sm.thr[qc] = keep_thr(c, rr.f1.y, eK);
       }
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp) {
@@ -178,6 +191,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
         const float dyA = pyA - A.x, dyB = dyA + 1.f, nb2 = A.y, nc = A.z, amp = A.w;
         const float fA = fmaf(dyA, fmaf(nc, dyA, Bq.y), Bq.x), fB = fmaf(dyB, fmaf(nc, dyB, Bq.y), Bq.x);
         const float gA = fmaf(nb2, dyA, Bq.z), gB = gA + nb2;   // log2 R at the first column
+        const float th = MK ? sm.thr[qe] : 0.f;
         if (bits >= 0) {
           float2 E2 = make_float2(vA ? amp * ex2(fA) : 0.f, vB ? amp * ex2(fB) : 0.f);
           float2 R2 = make_float2(vA ? ex2(gA) : 0.f, vB ? ex2(gB) : 0.f);
@@ -185,7 +199,12 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
 #pragma unroll
           for (int k = 0; k < T; ++k) {
             if (k >= k0 && k <= k1) {
-              acc[k] = __fadd2_rn(acc[k], E2);
+              if (MK) {
+                acc[k].x += E2.x >= th ? E2.x : 0.f;
+                acc[k].y += E2.y >= th ? E2.y : 0.f;
+              } else {
+                acc[k] = __fadd2_rn(acc[k], E2);
+              }
               E2 = __fmul2_rn(E2, R2);
               R2 = __fmul2_rn(R2, S2);
             }
@@ -196,8 +215,14 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
           for (int k = 0; k < T; ++k) {
             if (k >= k0 && k <= k1) {
               const float kf = (float)(k - k0), kq = kf * (kf - 1.f) * na;
-              if (vA) acc[k].x = fmaf(amp, ex2(fmaf(kf, gA, fA) + kq), acc[k].x);
-              if (vB) acc[k].y = fmaf(amp, ex2(fmaf(kf, gB, fB) + kq), acc[k].y);
+              if (MK) {
+                const float xa = amp * ex2(fmaf(kf, gA, fA) + kq), xb = amp * ex2(fmaf(kf, gB, fB) + kq);
+                if (vA && fabsf(xa) >= th) acc[k].x += xa;
+                if (vB && fabsf(xb) >= th) acc[k].y += xb;
+              } else {
+                if (vA) acc[k].x = fmaf(amp, ex2(fmaf(kf, gA, fA) + kq), acc[k].x);
+                if (vB) acc[k].y = fmaf(amp, ex2(fmaf(kf, gB, fB) + kq), acc[k].y);
+              }
             }
           }
         }
@@ -239,6 +264,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
 // coalesced store, no atomics; k_bwd_reduce sums over i in a fixed order (deterministic).
 constexpr int kBwdBlock = 256;
 
+template <bool MK>
 __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, const SplatRec *__restrict__ rec,
                                                           const float *__restrict__ dldi, float4 *__restrict__ slotA,
                                                           float2 *__restrict__ slotB) {
@@ -263,6 +289,8 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, const SplatR
   const float f0 = fmaf(dy0, fmaf(nc, dy0, Gx), Fx), f1 = fmaf(dyl, fmaf(nc, dyl, Gx), Fx);
   const float r0 = fmaf(nb2, dy0, D0), r1 = fmaf(nb2, dyl, D0);
   const bool slow = !(fminf(f0, f1) >= -100.f && fminf(r0, r1) >= -120.f && nc >= -60.f && fabsf(nb2) <= 120.f);
+  // MK: keep a pixel iff e >= ethr (= thr / |amp|, see keep_thr)
+  const float ethr = MK ? keep_thr(c, amp, ex2(nh * c.k * c.k)) / fabsf(amp) : 0.f;
   const float *gi = dldi + ((size_t)i * c.D + vlo) * c.D + ulo;
   float M0 = 0.f, M1 = 0.f, M2 = 0.f, Y0 = 0.f, Y1 = 0.f, YY = 0.f;
   float El = 0.f, V = 0.f, Rl = 0.f, W = 0.f, Kb = 0.f, S = 0.f;
@@ -294,7 +322,8 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, const SplatR
       // L1 requests); an odd first column and an odd last column are peeled
       int k = 0;
       auto step = [&](float gA, float gBv) {
-        const float2 h = __fmul2_rn(make_float2(gA, gBv), E2);
+        const float2 Em = MK ? make_float2(E2.x >= ethr ? E2.x : 0.f, E2.y >= ethr ? E2.y : 0.f) : E2;
+        const float2 h = __fmul2_rn(make_float2(gA, gBv), Em);
         const float2 hk = __fmul2_rn(h, kk);
         T0 = __fadd2_rn(T0, h);
         T1 = __fadd2_rn(T1, hk);
@@ -321,8 +350,10 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, const SplatR
 #pragma unroll 1
       for (int k = 0; k < wd; ++k) {
         const float kf = (float)k, kq = kf * (kf - 1.f) * na;
-        const float hA = __ldg(ga + k) * ex2(fmaf(kf, gA, fA) + kq);
-        const float hB = vB ? __ldg(gb + k) * ex2(fmaf(kf, gB, fB) + kq) : 0.f;
+        float eA = ex2(fmaf(kf, gA, fA) + kq), eB = ex2(fmaf(kf, gB, fB) + kq);
+        if (MK) { eA = eA >= ethr ? eA : 0.f; eB = eB >= ethr ? eB : 0.f; }
+        const float hA = __ldg(ga + k) * eA;
+        const float hB = vB ? __ldg(gb + k) * eB : 0.f;
         T0.x += hA; T0.y += hB;
         T1.x = fmaf(hA, kf, T1.x); T1.y = fmaf(hB, kf, T1.y);
         T2.x = fmaf(hA * kf, kf, T2.x); T2.y = fmaf(hB * kf, kf, T2.y);
@@ -428,28 +459,37 @@ int persistent_grid(K kern, int threads, size_t smem) {
   return sms * (b > 0 ? b : 1);
 }
 
-template <int T>
+template <int T, bool MK>
 void launch_fwd_t(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
                   int *ticket, cudaStream_t s) {
   static int grid = 0;
   const size_t smem = sizeof(FwdSmem<T>) * kFwdWarps;
-  if (!grid) grid = persistent_grid(k_render_fwd<T>, kFwdWarps * 32, smem);
-  k_render_fwd<T><<<grid, kFwdWarps * 32, smem, s>>>(c, B, rec, base, ids, proj, ticket);
+  if (!grid) grid = persistent_grid(k_render_fwd<T, MK>, kFwdWarps * 32, smem);
+  k_render_fwd<T, MK><<<grid, kFwdWarps * 32, smem, s>>>(c, B, rec, base, ids, proj, ticket);
 }
+
+bool pixel_mask(const CfgDev &c) { return (c.flags & (GEM_FLAG_ELLIPSE | GEM_FLAG_PIXEL_TAU)) != 0; }
 
 }  // namespace
 
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
                        int *ticket, cudaStream_t s, int &launches) {
-  if (c.T == 16) launch_fwd_t<16>(c, B, rec, base, ids, proj, ticket, s);
-  else launch_fwd_t<8>(c, B, rec, base, ids, proj, ticket, s);
+  const bool mk = pixel_mask(c);
+  if (c.T == 16) {
+    if (mk) launch_fwd_t<16, true>(c, B, rec, base, ids, proj, ticket, s);
+    else launch_fwd_t<16, false>(c, B, rec, base, ids, proj, ticket, s);
+  } else {
+    if (mk) launch_fwd_t<8, true>(c, B, rec, base, ids, proj, ticket, s);
+    else launch_fwd_t<8, false>(c, B, rec, base, ids, proj, ticket, s);
+  }
   ++launches;
 }
 
 void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float *dldi, float4 *slotA, float2 *slotB,
                        cudaStream_t s, int &launches) {
   dim3 grid((c.N + kBwdBlock - 1) / kBwdBlock, B);
-  k_render_bwd<<<grid, kBwdBlock, 0, s>>>(c, rec, dldi, slotA, slotB);
+  if (pixel_mask(c)) k_render_bwd<true><<<grid, kBwdBlock, 0, s>>>(c, rec, dldi, slotA, slotB);
+  else k_render_bwd<false><<<grid, kBwdBlock, 0, s>>>(c, rec, dldi, slotA, slotB);
   ++launches;
 }
 

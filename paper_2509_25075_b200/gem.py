@@ -36,6 +36,7 @@ class GemConfig:
     wave: int = 0         # particles per wave (0 = auto)
     ablation: str = "full"   # Table 5: full | no_rotation | isotropic_scale | both
     zsort: bool = False      # P:227 z-sorted per-tile lists (GEM_FLAG_ZSORT)
+    pixel_mask: str = "aabb"  # Eq. 8 per-pixel selection: aabb | ellipse | tau | ellipse+tau
 
     def c(self) -> _b.GemConfigC:
         return _b.GemConfigC(self.D, self.pixel_size, self.n_gauss, self.max_batch, self.cull_k, self.tau, self.tile,
@@ -48,6 +49,12 @@ class GemConfig:
         f = _b.GEM_FLAG_FUSED if self.fused else 0
         if self.zsort:
             f |= _b.GEM_FLAG_ZSORT
+        if self.pixel_mask not in ("aabb", "ellipse", "tau", "ellipse+tau"):
+            raise ValueError(f"unknown pixel_mask {self.pixel_mask!r}")
+        if "ellipse" in self.pixel_mask:
+            f |= _b.GEM_FLAG_ELLIPSE
+        if "tau" in self.pixel_mask:
+            f |= _b.GEM_FLAG_PIXEL_TAU
         if self.ablation in ("no_rotation", "both"):
             f |= _b.GEM_FLAG_NO_ROTATION
         if self.ablation in ("isotropic_scale", "both"):
