@@ -252,6 +252,164 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
   retire(ticket, lane);
 }
 
+// Forward for 8x8 tiles, lane per entry.  Every lane keeps a private copy of the whole tile in
+// registers (4 row pairs x 8 columns, packed fp32x2 = 64 floats) and renders whole list entries,
+// lane l taking entries l, l + 32, ... of the tile (records prefetched one round ahead, ids two):
+// no binning, no shared memory, no idle lanes except in a tile's last round.  An entry walks the
+// row pairs its box covers (predicated, fully unrolled) with the recurrences of the forward
+// comment extended down the column in pairs: with E2 = (e_r, e_r+1) at the first column,
+//   E2 <- E2 (V_r^2 W, V_r^2 W^3),  (V_r^2 W, V_r^2 W^3) <- (.) W^4,  R2 <- R2 Kb^2  per row pair,
+// so an entry costs 6 exps.  The 32 private copies are summed by a fixed reduce-scatter of
+// shuffles (halving 64 -> 2 values per lane; lane L ends with row pair L / 8, column L % 8):
+// bitwise deterministic.  The row-pair recurrence squares V, so entries with |log2 V| > 60 at
+// an end row take the direct path too.
+constexpr int kLeWarps = 2;
+
+template <bool MK>
+__global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, int B, const SplatRec *__restrict__ rec,
+                                                                    const int *__restrict__ base,
+                                                                    const int *__restrict__ ids,
+                                                                    float *__restrict__ proj, int *ticket) {
+  constexpr int T = 8;
+  constexpr float nh = -0.5f * kLog2e;
+  const float eK = MK ? ex2(nh * c.k * c.k) : 0.f;
+  const int lane = threadIdx.x & 31;
+  const int items = B * c.NT;
+  auto bounds = [&](int it, int &s_, int &e_) {
+    s_ = 0; e_ = 0;
+    if (it < items) {
+      const int ii = it / c.NT, tt = it - ii * c.NT;
+      const size_t h = ((size_t)ii * c.NT + tt) * c.C;
+      s_ = base[h];
+      e_ = base[h + c.C];
+    }
+  };
+  int nitem = next_item(ticket, lane), ns, ne;
+  bounds(nitem, ns, ne);
+  for (;;) {
+    const int item = nitem;
+    if (item >= items) break;
+    int s = ns, e = ne;
+    nitem = next_item(ticket, lane);
+    bounds(nitem, ns, ne);
+    const int i = item / c.NT, t = item - i * c.NT;
+    const int u0 = (t % c.nt) * T, v0 = (t / c.nt) * T;
+    if ((int64_t)e > c.cap) e = (int)c.cap;
+    if ((int64_t)s > c.cap) s = (int)c.cap;
+    float *out = proj + (size_t)i * c.D * c.D;
+    if (s >= e) {   // empty tile: the projection is zero there
+      for (int p = lane; p < T * T; p += 32) {
+        const int u = u0 + p % T, v = v0 + p / T;
+        if (u < c.D && v < c.D) out[(size_t)v * c.D + u] = 0.f;
+      }
+      continue;
+    }
+    float2 acc[4][T];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int k = 0; k < T; ++k) acc[p][k] = make_float2(0.f, 0.f);
+    const SplatRec *reci = rec + (size_t)i * c.N;
+    const int nall = e - s;
+    int id2 = 32 + lane < nall ? ids[s + 32 + lane] : 0;
+    SplatRec nxt;
+    if (lane < nall) nxt = reci[ids[s + lane]];
+    for (int g0 = 0; g0 < nall; g0 += 32) {
+      const int q = g0 + lane;
+      const SplatRec rr = nxt;
+      if (q + 32 < nall) nxt = reci[id2];
+      if (q + 64 < nall) id2 = ids[s + q + 64];
+      if (q >= nall) continue;
+      const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
+      const int ulo = (ub & 0xffff) - u0, uhi = (ub >> 16) - u0, vlo = (vb & 0xffff) - v0, vhi = (vb >> 16) - v0;
+      const int cu0 = max(ulo, 0), cu1 = min(uhi, T - 1), cv0 = max(vlo, 0), cv1 = min(vhi, T - 1);
+      const int p0 = cv0 >> 1, p1 = cv1 >> 1;
+      const float na = nh * rr.f0.z, nb2 = 2.f * nh * rr.f0.w, nc = nh * rr.f1.x, amp = rr.f1.y;
+      const float mx = (float)ulo + rr.f0.x, my = (float)vlo + rr.f0.y;
+      const float dx0 = (float)cu0 - mx, dyS = (float)(2 * p0) - my, dyE = (float)(2 * p1 + 1) - my;
+      // log2 of: e at (cu0, dy); R = e(k+1)/e(k) at cu0; V = e(r+1)/e(r) at cu0
+      const float Fx = na * dx0 * dx0, Gx = nb2 * dx0;
+      const float fS = fmaf(dyS, fmaf(nc, dyS, Gx), Fx), fE = fmaf(dyE, fmaf(nc, dyE, Gx), Fx);
+      const float D0 = na * fmaf(2.f, dx0, 1.f);
+      const float gS = fmaf(nb2, dyS, D0), gE = fmaf(nb2, dyE, D0);
+      const float hS = fmaf(nc, fmaf(2.f, dyS, 1.f), Gx), hE = fmaf(nc, fmaf(2.f, dyE, 1.f), Gx);
+      const bool slow = !(fminf(fS, fE) >= -100.f && fminf(gS, gE) >= -120.f && fmaxf(fabsf(hS), fabsf(hE)) <= 60.f &&
+                          nc >= -30.f && fabsf(nb2) <= 60.f && amp > 0.f);
+      const float th = MK ? keep_thr(c, amp, eK) : 0.f;
+      if (!slow) {
+        const float EA = amp * ex2(fS), VA = ex2(hS), RA = ex2(gS);
+        const float W = ex2(2.f * nc), Kb = ex2(nb2), S = ex2(2.f * na);
+        float2 E2 = make_float2(EA, EA * VA), R2 = make_float2(RA, RA * Kb);
+        const float VVW = VA * VA * W, W2 = W * W;
+        float2 VV2 = make_float2(VVW, VVW * W2);
+        const float2 W42 = make_float2(W2 * W2, W2 * W2), Kb22 = make_float2(Kb * Kb, Kb * Kb), S2 = make_float2(S, S);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          if (p >= p0 && p <= p1) {
+            float2 Em = make_float2(2 * p >= cv0 ? E2.x : 0.f, 2 * p + 1 <= cv1 ? E2.y : 0.f);
+            float2 Rc = R2;
+#pragma unroll
+            for (int k = 0; k < T; ++k) {
+              if (k >= cu0 && k <= cu1) {
+                if (MK) {
+                  acc[p][k].x += Em.x >= th ? Em.x : 0.f;
+                  acc[p][k].y += Em.y >= th ? Em.y : 0.f;
+                } else {
+                  acc[p][k] = __fadd2_rn(acc[p][k], Em);
+                }
+                Em = __fmul2_rn(Em, Rc);
+                Rc = __fmul2_rn(Rc, S2);
+              }
+            }
+            E2 = __fmul2_rn(E2, VV2);
+            VV2 = __fmul2_rn(VV2, W42);
+            R2 = __fmul2_rn(R2, Kb22);
+          }
+        }
+      } else {   // direct evaluation, exp per pixel
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          if (p >= p0 && p <= p1) {
+            const float dyA = (float)(2 * p) - my, dyB = dyA + 1.f;
+            const bool vA = 2 * p >= cv0, vB = 2 * p + 1 <= cv1;
+#pragma unroll
+            for (int k = 0; k < T; ++k) {
+              if (k >= cu0 && k <= cu1) {
+                const float dx = (float)k - mx;
+                const float fa = fmaf(dx, fmaf(na, dx, nb2 * dyA), nc * dyA * dyA);
+                const float fb = fmaf(dx, fmaf(na, dx, nb2 * dyB), nc * dyB * dyB);
+                const float xa = amp * ex2(fa), xb = amp * ex2(fb);
+                if (vA && (!MK || fabsf(xa) >= th)) acc[p][k].x += xa;
+                if (vB && (!MK || fabsf(xb) >= th)) acc[p][k].y += xb;
+              }
+            }
+          }
+        }
+      }
+    }
+    // reduce-scatter of the 32 private tiles: flattened index n = 16 p + 2 k + (0: .x, 1: .y);
+    // after halving on lane bits 16, 8, 4, 2, 1 lane L holds n = 2L, 2L + 1
+    float v[64];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int k = 0; k < T; ++k) { v[16 * p + 2 * k] = acc[p][k].x; v[16 * p + 2 * k + 1] = acc[p][k].y; }
+#pragma unroll
+    for (int o = 16, h = 32; o >= 1; o >>= 1, h >>= 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int n = 0; n < h; ++n) {
+        const float keep = up ? v[n + h] : v[n], send = up ? v[n] : v[n + h];
+        v[n] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    const int u = u0 + (lane & 7), vr = v0 + 2 * (lane >> 3);
+    if (u < c.D && vr < c.D) out[(size_t)vr * c.D + u] = v[0];
+    if (u < c.D && vr + 1 < c.D) out[(size_t)(vr + 1) * c.D + u] = v[1];
+  }
+  retire(ticket, lane);
+}
+
 // Backward ("gradient computation restricted to the Gaussians contributing to each pixel",
 // PAPER.md:108, :117), Gaussian-parallel: one thread per (particle i, Gaussian j) with a
 // non-empty AABB walks the whole box (no tiles, no lists) with the forward's recurrences,
@@ -475,7 +633,14 @@ bool pixel_mask(const CfgDev &c) { return (c.flags & (GEM_FLAG_ELLIPSE | GEM_FLA
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
                        int *ticket, cudaStream_t s, int &launches) {
   const bool mk = pixel_mask(c);
-  if (c.T == 16) {
+  if (c.T == 8) {
+    static int grid[2] = {0, 0};
+    int &g = grid[mk ? 1 : 0];
+    if (!g) g = mk ? persistent_grid(k_render_fwd_le<true>, kLeWarps * 32, 0)
+                   : persistent_grid(k_render_fwd_le<false>, kLeWarps * 32, 0);
+    if (mk) k_render_fwd_le<true><<<g, kLeWarps * 32, 0, s>>>(c, B, rec, base, ids, proj, ticket);
+    else k_render_fwd_le<false><<<g, kLeWarps * 32, 0, s>>>(c, B, rec, base, ids, proj, ticket);
+  } else if (c.T == 16) {
     if (mk) launch_fwd_t<16, true>(c, B, rec, base, ids, proj, ticket, s);
     else launch_fwd_t<16, false>(c, B, rec, base, ids, proj, ticket, s);
   } else {
