@@ -31,6 +31,8 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   d.tshift = c.tile == 16 ? 4 : 3;
   d.nt = (c.D + c.tile - 1) / c.tile;
   d.NT = d.nt * d.nt;
+  d.inv_NT = 1.0f / (float)d.NT;
+  d.inv_nt = 1.0f / (float)d.nt;
   d.N = (int)c.n_gauss;
   d.C = (d.N + kChunk - 1) / kChunk;
   d.px = c.pixel_size;

@@ -61,7 +61,17 @@ struct CfgDev {        // resolved config passed by value to kernels
   unsigned flags;                   // gem_config.flags
   float px, k, tau;
   int64_t cap;
+  float inv_NT, inv_nt;             // 1 / NT, 1 / nt (fast exact division, see fdivmod)
 };
+
+// q = x / d, r = x % d for 0 <= x < 2^22 with a float reciprocal and an exact correction
+__device__ __forceinline__ int fdivmod(int x, int d, float inv, int &r) {
+  int q = __float2int_rz((float)x * inv);
+  r = x - q * d;
+  while (r < 0) { --q; r += d; }
+  while (r >= d) { ++q; r -= d; }
+  return q;
+}
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
 // shuffles (halving 64 -> 2 values per lane; lane L ends with row pair L / 8, column L % 8):
 // bitwise deterministic.  The row-pair recurrence squares V, so entries with |log2 V| > 60 at
 // an end row take the direct path too.
-constexpr int kLeWarps = 2;
+constexpr int kLeWarps = 2, kLeBatch = 4;
 
 template <bool MK>
 __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, int B, const SplatRec *__restrict__ rec,
@@ -275,25 +275,33 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
   const float eK = MK ? ex2(nh * c.k * c.k) : 0.f;
   const int lane = threadIdx.x & 31;
   const int items = B * c.NT;
+  // items (particle, tile) are taken kLeBatch at a time from the ticket; the next item's list
+  // bounds are fetched while the current one is rendered
   auto bounds = [&](int it, int &s_, int &e_) {
     s_ = 0; e_ = 0;
     if (it < items) {
-      const int ii = it / c.NT, tt = it - ii * c.NT;
-      const size_t h = ((size_t)ii * c.NT + tt) * c.C;
+      const size_t h = (size_t)it * c.C;   // it = i * NT + t
       s_ = base[h];
       e_ = base[h + c.C];
     }
   };
-  int nitem = next_item(ticket, lane), ns, ne;
+  int bat = kLeBatch * next_item(ticket, lane), pos = 0;
+  auto take = [&]() {
+    if (pos == kLeBatch) { bat = kLeBatch * next_item(ticket, lane); pos = 0; }
+    return bat + pos++;
+  };
+  int nitem = take(), ns, ne;
   bounds(nitem, ns, ne);
   for (;;) {
     const int item = nitem;
     if (item >= items) break;
     int s = ns, e = ne;
-    nitem = next_item(ticket, lane);
+    nitem = take();
     bounds(nitem, ns, ne);
-    const int i = item / c.NT, t = item - i * c.NT;
-    const int u0 = (t % c.nt) * T, v0 = (t / c.nt) * T;
+    int t, tu;
+    const int i = fdivmod(item, c.NT, c.inv_NT, t);
+    const int tv = fdivmod(t, c.nt, c.inv_nt, tu);
+    const int u0 = tu * T, v0 = tv * T;
     if ((int64_t)e > c.cap) e = (int)c.cap;
     if ((int64_t)s > c.cap) s = (int)c.cap;
     float *out = proj + (size_t)i * c.D * c.D;
@@ -324,6 +332,7 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
       const int ulo = (ub & 0xffff) - u0, uhi = (ub >> 16) - u0, vlo = (vb & 0xffff) - v0, vhi = (vb >> 16) - v0;
       const int cu0 = max(ulo, 0), cu1 = min(uhi, T - 1), cv0 = max(vlo, 0), cv1 = min(vhi, T - 1);
       const int p0 = cv0 >> 1, p1 = cv1 >> 1;
+      const unsigned cm = (0xffu << cu0) & (0xffu >> (T - 1 - cu1));   // covered columns
       const float na = nh * rr.f0.z, nb2 = 2.f * nh * rr.f0.w, nc = nh * rr.f1.x, amp = rr.f1.y;
       const float mx = (float)ulo + rr.f0.x, my = (float)vlo + rr.f0.y;
       const float dx0 = (float)cu0 - mx, dyS = (float)(2 * p0) - my, dyE = (float)(2 * p1 + 1) - my;
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
             float2 Rc = R2;
 #pragma unroll
             for (int k = 0; k < T; ++k) {
-              if (k >= cu0 && k <= cu1) {
+              if (cm & (1u << k)) {
                 if (MK) {
                   acc[p][k].x += Em.x >= th ? Em.x : 0.f;
                   acc[p][k].y += Em.y >= th ? Em.y : 0.f;
