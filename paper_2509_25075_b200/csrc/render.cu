@@ -352,24 +352,28 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
         const float VVW = VA * VA * W, W2 = W * W;
         float2 VV2 = make_float2(VVW, VVW * W2);
         const float2 W42 = make_float2(W2 * W2, W2 * W2), Kb22 = make_float2(Kb * Kb, Kb * Kb), S2 = make_float2(S, S);
+        // all four row pairs run predicated (no branches: the pairs' column chains are
+        // independent and interleave); pairs outside [p0, p1] add zeros, and the row-pair
+        // recurrence only advances inside [p0, p1], so every factor stays finite
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          if (p >= p0 && p <= p1) {
-            float2 Em = make_float2(2 * p >= cv0 ? E2.x : 0.f, 2 * p + 1 <= cv1 ? E2.y : 0.f);
-            float2 Rc = R2;
+          const bool inr = p >= p0 && p <= p1;
+          float2 Em = make_float2(inr && 2 * p >= cv0 ? E2.x : 0.f, inr && 2 * p + 1 <= cv1 ? E2.y : 0.f);
+          float2 Rc = R2;
 #pragma unroll
-            for (int k = 0; k < T; ++k) {
-              if (cm & (1u << k)) {
-                if (MK) {
-                  acc[p][k].x += Em.x >= th ? Em.x : 0.f;
-                  acc[p][k].y += Em.y >= th ? Em.y : 0.f;
-                } else {
-                  acc[p][k] = __fadd2_rn(acc[p][k], Em);
-                }
-                Em = __fmul2_rn(Em, Rc);
-                Rc = __fmul2_rn(Rc, S2);
+          for (int k = 0; k < T; ++k) {
+            if (cm & (1u << k)) {
+              if (MK) {
+                acc[p][k].x += Em.x >= th ? Em.x : 0.f;
+                acc[p][k].y += Em.y >= th ? Em.y : 0.f;
+              } else {
+                acc[p][k] = __fadd2_rn(acc[p][k], Em);
               }
+              Em = __fmul2_rn(Em, Rc);
+              Rc = __fmul2_rn(Rc, S2);
             }
+          }
+          if (p >= p0 && p < p1) {   // advance only between covered pairs: no overflow
             E2 = __fmul2_rn(E2, VV2);
             VV2 = __fmul2_rn(VV2, W42);
             R2 = __fmul2_rn(R2, Kb22);
