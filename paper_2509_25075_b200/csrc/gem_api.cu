@@ -87,7 +87,7 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.hist = take(sizeof(int) * (size_t)L.n_hist);
   L.subcnt = take(sizeof(int) * (size_t)L.n_hist * 4);   // per fill-warp sub-chunk tile counts
   L.base = take(sizeof(int) * ((size_t)L.n_hist + 1));
-  L.scan_blk = take(sizeof(int) * ((size_t)L.n_scan_blk + 1));
+  L.scan_blk = take(sizeof(unsigned long long) * ((size_t)L.n_scan_blk + 1));   // scan look-back state
   L.ids = take(sizeof(int) * (size_t)L.list_cap);
   L.proj = take(sizeof(float) * W * D * D);
   L.spec_hat = take(sizeof(float2) * W * H);
@@ -275,6 +275,8 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
   if (st != GEM_OK) { gem_destroy(ctx); return st; }
   if (cudaMemsetAsync(ctx->ws + L.stats, 0, sizeof(DevStats), ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(ctx->ws + L.ticket, 0, 64, ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(ctx->ws + L.scan_blk, 0, sizeof(unsigned long long) * ((size_t)L.n_scan_blk + 1), ctx->stream) !=
+          cudaSuccess ||
       cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
     gem_destroy(ctx);
     return GEM_E_CUDA;
@@ -400,7 +402,12 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist, at<int>(ctx, L.subcnt), st, s,
                          ctx->launches); }
     const int64_t nh = (int64_t)nb * c.NT * c.C;
-    { Prof p(ctx, s, P_SCAN); launch_scan(hist, base, nh, at<int>(ctx, L.scan_blk), (nh + 4095) / 4096, st, c.cap, s, ctx->launches); }
+    {
+      Prof p(ctx, s, P_SCAN);
+      launch_scan_1p(hist, base, nh, at<unsigned long long>(ctx, L.scan_blk), (nh + 4095) / 4096,
+                     ctx->scan_epoch = ctx->scan_epoch % 0x3ffffffeu + 1u,   // 1 .. 2^30 - 1 (state zeroed at init)
+                     at<int>(ctx, L.ticket) + 8, st, c.cap, s, ctx->launches);
+    }
     uint2 *zpair = (c.flags & GEM_FLAG_ZSORT) ? at<uint2>(ctx, L.zs_key) : nullptr;
     { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<int>(ctx, L.subcnt), ids, (const float4 *)params->mean_rho, rw, zpair, s, ctx->launches); }
     if (zpair) {

@@ -96,6 +96,7 @@ struct gem_ctx {
   int fused;           // GEM_FLAG_FUSED
   int last_p0, last_nb;  // the last wave of the last forward
   int launches;
+  unsigned scan_epoch;   // launch epoch of the single-pass scan's state words
   // profiling (gem_profile_enable): event pairs around launches
   int prof_on;
   int prof_n, prof_cap;
@@ -129,6 +130,8 @@ void launch_prep(const CfgDev &c, const float4 *log_scale, const float4 *quat, G
 void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
                         const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, DevStats *st,
                         cudaStream_t s, int &launches);
+void launch_scan_1p(const int *in, int *out, int64_t n, unsigned long long *state, int64_t nblk, unsigned epoch,
+                    int *tk, DevStats *st, int64_t cap, cudaStream_t s, int &launches);
 void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, DevStats *st, int64_t cap, cudaStream_t s,
                  int &launches);
 void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,

@@ -355,6 +355,84 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int *__restrict__ out
     if (base + k < n) out[base + k] += add;
 }
 
+// Single-pass exclusive scan (decoupled look-back): blocks take tiles in launch order from a
+// ticket, scan their tile, publish the tile aggregate, and thread 0 walks back over the
+// predecessors' published words (aggregate or inclusive prefix) until it meets an inclusive
+// prefix.  Words carry the launch epoch, so the state array needs no reset; the ticket resets
+// itself (last block out).  The last tile writes out[n] = total and the stats.
+constexpr int k1pThreads = 1024, k1pItems = 4, k1pTile = k1pThreads * k1pItems;
+
+__global__ void __launch_bounds__(k1pThreads) k_scan_1p(const int *__restrict__ in, int *__restrict__ out, int64_t n,
+                                                          int64_t nblk, unsigned long long *state, unsigned epoch,
+                                                          int *tk, DevStats *st, int64_t cap) {
+  __shared__ int sw[33];
+  __shared__ int s_bid, s_prefix;
+  if (threadIdx.x == 0) s_bid = atomicAdd(tk, 1);
+  __syncthreads();
+  const int bid = s_bid;
+  const int64_t base = (int64_t)bid * k1pTile + (int64_t)threadIdx.x * k1pItems;
+  int v[k1pItems], s = 0;
+#pragma unroll
+  for (int k = 0; k < k1pItems; ++k) {
+    v[k] = (base + k < n) ? in[base + k] : 0;
+    s += v[k];
+  }
+  int total;
+  int e = block_excl_scan(s, sw, total);
+  const unsigned long long ep = (unsigned long long)(epoch & 0x3fffffffu) << 34;
+  volatile unsigned long long *vs = state;
+  if (threadIdx.x < 32) {   // warp 0: publish the aggregate, then look back 32 predecessors at a time
+    const int lane = threadIdx.x;
+    int prefix = 0;
+    if (bid > 0) {
+      if (lane == 0) {
+        vs[bid] = ep | (1ull << 32) | (unsigned)total;   // aggregate
+        __threadfence();
+      }
+      for (int j0 = bid - 1;;) {
+        const int j = j0 - lane;
+        unsigned long long w = 0;
+        bool ready = true;
+        if (j >= 0) {
+          w = vs[j];
+          ready = (w >> 34) == (ep >> 34);
+        }
+        if (!__all_sync(0xffffffffu, ready)) continue;        // some predecessor not published yet
+        const unsigned pmask = __ballot_sync(0xffffffffu, j >= 0 && ((w >> 32) & 3u) == 2u);
+        const int stop = pmask ? __ffs(pmask) - 1 : 31;       // nearest inclusive prefix in the window
+        int val = (j >= 0 && lane <= stop) ? (int)(unsigned)w : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        prefix += val;
+        if (pmask || j0 - 31 <= 0) break;
+        j0 -= 32;
+      }
+    }
+    if (lane == 0) {
+      __threadfence();
+      vs[bid] = ep | (2ull << 32) | (unsigned)(prefix + total);   // inclusive prefix
+      s_prefix = prefix;
+    }
+  }
+  __syncthreads();
+  e += s_prefix;
+#pragma unroll
+  for (int k = 0; k < k1pItems; ++k) {
+    if (base + k < n) out[base + k] = e;
+    e += v[k];
+  }
+  if (threadIdx.x == 0) {
+    if (bid == nblk - 1) {   // totals accumulate over the waves of one forward
+      const int tot = s_prefix + total;
+      out[n] = tot;
+      st->entries += (unsigned long long)tot;
+      if ((int64_t)tot > cap) st->overflow = 1;
+    }
+    __threadfence();
+    if (atomicAdd(tk + 1, 1) == (int)nblk - 1) { tk[0] = 0; tk[1] = 0; }
+  }
+}
+
 // --------------------------------------------------------------- a3 fill
 // One CTA of 4 warps per (particle, chunk of kChunk Gaussians); warp w owns the sub-chunk w.
 // Pass 1 counts each sub-chunk's entries per tile (smem integer atomics, order-free); a per-tile
@@ -463,6 +541,12 @@ void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, Dev
   k_scan_blocks<<<1, kScanThreads, 0, s>>>(blk, nblk, out, n, st, cap);
   k_scan_add<<<(unsigned)nblk, kScanThreads, 0, s>>>(out, n, blk);
   launches += 3;
+}
+
+void launch_scan_1p(const int *in, int *out, int64_t n, unsigned long long *state, int64_t nblk, unsigned epoch,
+                    int *tk, DevStats *st, int64_t cap, cudaStream_t s, int &launches) {
+  k_scan_1p<<<(unsigned)nblk, k1pThreads, 0, s>>>(in, out, n, nblk, state, epoch, tk, st, cap);
+  ++launches;
 }
 
 void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,
