@@ -104,23 +104,28 @@ class ClockSampler:
         h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu_index)
         self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         while True:
-            self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
             r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            for name, bit in self.REASONS.items():
-                if r & bit:
-                    self.reasons.add(name)
-            if self._stop.wait(0.005):
+            self.samples.append((time.perf_counter(), mhz, r))
+            self._ready.set()
+            if self._stop.wait(0.002):
                 break
 
     def __enter__(self):
+        self._ready = threading.Event()
         try:
             import pynvml
             pynvml.nvmlInit()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            self._ready.wait(timeout=5)   # sampling runs before the timed region starts
         except Exception:
             self.t = None
         return self
+
+    def mark(self, which):
+        """Host time of the timed region's start / end (samples outside it are dropped)."""
+        setattr(self, which, time.perf_counter())
 
     def __exit__(self, *a):
         self._stop.set()
@@ -128,10 +133,16 @@ class ClockSampler:
             self.t.join(timeout=2)
 
     def summary(self):
-        if not self.samples:
+        t0, t1 = getattr(self, "start", None), getattr(self, "end", None)
+        inside = [x for x in self.samples if t0 is None or t1 is None or t0 <= x[0] <= t1]
+        if not inside and self.samples:   # region shorter than the sampling period: nearest sample
+            mid = 0.5 * (t0 + t1) if t0 is not None and t1 is not None else self.samples[-1][0]
+            inside = [min(self.samples, key=lambda x: abs(x[0] - mid))]
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        reasons = sorted({name for _, _, r in inside for name, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(m for _, m, _ in inside), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(inside)}
 
 
 # --------------------------------------------------------------- CPU oracle
@@ -270,11 +281,13 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        clk.mark("start")
         ev0.record(stream)
         for k in range(args.steps):
             step(args.warmup + k)
         ev1.record(stream)
         torch.cuda.synchronize()
+        clk.mark("end")
         if world > 1:
             dist.barrier()
     launches = sc.launches - launches0

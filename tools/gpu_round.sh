@@ -18,6 +18,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_r
 python tools/ncu_summary.py gpurun_out/round/full_$TAG.ncu-rep 40 > gpurun_out/round/ncu_full_summary_$TAG.txt 2>&1
 python tools/ncu_stalls.py gpurun_out/round/full_$TAG.ncu-rep >> gpurun_out/round/ncu_full_summary_$TAG.txt 2>&1
 tail -2 gpurun_out/round/pytest_gpu.log; tail -2 gpurun_out/round/smoke.log; cat gpurun_out/round/bench_$TAG.json; cat gpurun_out/round/bench_ref_$TAG.json; tail -3 gpurun_out/round/bench_$TAG.err
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_render_bwd|k_bwd_reduce|k_splat_count|k_fill" -s 4 -c 4 -o gpurun_out/round/full2_$TAG $CMD > gpurun_out/round/ncu_full2.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_render_bwd" -s 1 -c 1 -o gpurun_out/round/full2_$TAG $CMD > gpurun_out/round/ncu_full2.log 2>&1
 python tools/ncu_summary.py gpurun_out/round/full2_$TAG.ncu-rep 40 > gpurun_out/round/ncu_full2_summary_$TAG.txt 2>&1
 python tools/ncu_stalls.py gpurun_out/round/full2_$TAG.ncu-rep >> gpurun_out/round/ncu_full2_summary_$TAG.txt 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_splat_count|k_fill" -s 2 -c 2 -o gpurun_out/round/full3_$TAG $CMD > gpurun_out/round/ncu_full3.log 2>&1
+python tools/ncu_summary.py gpurun_out/round/full3_$TAG.ncu-rep 40 > gpurun_out/round/ncu_full3_summary_$TAG.txt 2>&1
