@@ -511,3 +511,32 @@ def test_pixel_mask_variants(gem, orc, variant):
     assert np.all(np.abs(lo[:-1] - o["loss"]) < LOSS_TOL * o["loss"])
     for name, cols in CLASSES.items():
         assert maxnorm_rel(g[:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+
+
+def test_X_config_sampled(gem, orc):
+    """Config X (500 000 Gaussians, D = 384: 48 x 48 tiles, a non-power-of-two tile grid):
+    particle 0's lists are bit-exact, 256 sampled pixels of two particles match the oracle's
+    per-pixel projection, and the batch gradient equals the sum of its halves' gradients."""
+    B = 4
+    case = make_case("X", B=B, seed=17)
+    w = case["w"]
+    g = run_gpu(gem, case, tile=8)
+    assert g["stats"]["status"] == 0, g["stats"]
+    sub0 = dict(case, rot=case["rot"][:1], shift=case["shift"][:1], ctf=case["ctf"][:1], obs=case["obs"][:1])
+    assert_lists_exact(orc, sub0, [g["st"].export_lists(0)], 8)
+    rng = np.random.default_rng(5)
+    pix = rng.integers(w.D // 4, 3 * w.D // 4, (256, 2)).astype(np.int32)   # mostly inside the object
+    for i in (0, 3):
+        ref = orc.project_pixels(case["params"], case["rot"][i], case["shift"][i], w.D, case["px"], pix)
+        got = g["proj"][i][pix[:, 1], pix[:, 0]]
+        full_max = np.abs(g["proj"][i]).max()
+        assert np.abs(got - ref).max() < IMG_TOL * full_max, i
+    assert np.all(np.isfinite(g["loss"]))
+    parts = []
+    for h in range(2):
+        sl = slice(2 * h, 2 * h + 2)
+        sub = dict(case, rot=case["rot"][sl], shift=case["shift"][sl], ctf=case["ctf"][sl], obs=case["obs"][sl])
+        parts.append(run_gpu(gem, sub, tile=8)["grad"].astype(np.float64))
+    tot = parts[0] + parts[1]
+    for name, cols in CLASSES.items():
+        assert maxnorm_rel(g["grad"][:, cols], tot[:, cols]) < 1e-5, name
