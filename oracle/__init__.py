@@ -51,6 +51,8 @@ def lib():
         _lib.orc_splats.argtypes = [i, i, p, p, p, p, p, i, d, d, d, p, p, p]
         _lib.orc_lists.restype = ll
         _lib.orc_lists.argtypes = [i, i, i, i, p, p, p, p, p, ll]
+        _lib.orc_lists_pixmask.restype = ll
+        _lib.orc_lists_pixmask.argtypes = [i, i, p, p, p, p, p, i, d, d, d, i, i, p, p, p, ll]
         _lib.orc_project.restype = None
         _lib.orc_project.argtypes = [i, i, p, p, p, p, p, i, d, d, d, i, p]
         _lib.orc_project_pixels.restype = None
@@ -124,6 +126,26 @@ def lists(aabb, visible, D, T):
     base = np.zeros(B, np.int64)
     ids = np.zeros(cap, np.int32)
     tot = lib().orc_lists(N, B, D, T, _ptr(aabb), _ptr(visible), _ptr(tile_off), _ptr(base), _ptr(ids), cap)
+    assert tot >= 0
+    return tile_off, base, ids[:tot].copy()
+
+
+# -------------------------------------------------------------------- O4m
+def lists_pixmask(params, rot, shift, D, px, T, pixmask, k=3.0, tau=0.0):
+    """O4m: tile lists of the per-pixel selection variants -- a tile lists Gaussian j only if a
+    pixel of tile x AABB_ij is kept (2: Q <= k^2, 4: |amp| exp(-Q/2) >= tau); ascending j.
+    Returns (tile_off[B, NT+1], ids_base[B], ids) like ``lists``."""
+    mr, ls, qu = (_f64(p) for p in params)
+    rot, shift = _f64(rot), _f64(shift)
+    N, B = mr.shape[0], rot.shape[0]
+    nt = (D + T - 1) // T
+    NT = nt * nt
+    cap = N * NT * B + 1
+    tile_off = np.zeros((B, NT + 1), np.int32)
+    base = np.zeros(B, np.int64)
+    ids = np.zeros(min(cap, 50_000_000), np.int32)
+    tot = lib().orc_lists_pixmask(N, B, _ptr(mr), _ptr(ls), _ptr(qu), _ptr(rot), _ptr(shift), D, px, k, tau, T,
+                                  int(pixmask), _ptr(tile_off), _ptr(base), _ptr(ids), ids.size)
     assert tot >= 0
     return tile_off, base, ids[:tot].copy()
 

@@ -210,6 +210,57 @@ long long orc_lists(int N, int B, int D, int T, const int32_t *aabb, const int32
   return total;
 }
 
+/* ----------------------------------------------------------------- O4m ---
+ * Tile lists for the per-pixel selection variants ("exact ellipse-tile
+ * intersection instead of the AABB"; reading L26): list(i,t) = { j visible : some pixel of
+ * tile t inside AABB_ij is kept by pix_keep (Q <= k^2 and/or |amp| exp(-Q/2) >= tau) },
+ * ascending j.  Brute force over the pixels of every tile x AABB intersection.  Same layout as
+ * orc_lists.  Defined after pix_keep below (forward declaration). */
+static int pix_keep(const orc_splat_t *s, double Q, int pixmask, double k, double tau);
+long long orc_lists_pixmask(int N, int B, const double *mean_rho, const double *log_scale, const double *quat,
+                            const double *rot, const double *shift, int D, double px, double k, double tau, int T,
+                            int pixmask, int32_t *tile_off, int64_t *ids_base, int32_t *ids, long long cap) {
+  orc_gauss_t *g = prep_all(N, quat, log_scale);
+  orc_splat_t *sp = (orc_splat_t *)malloc((size_t)B * N * sizeof(orc_splat_t));
+  for (int i = 0; i < B; ++i)
+    for (int j = 0; j < N; ++j)
+      orc_splat(rot + 9 * i, shift + 2 * i, mean_rho + 4 * j, g[j].Sig, g[j].detS, mean_rho[4 * j + 3], g[j].ok, px,
+                D, k, tau, &sp[(size_t)i * N + j]);
+  int nt = (D + T - 1) / T, NT = nt * nt;
+  double half = (double)(D / 2);
+  long long total = 0;
+  for (int i = 0; i < B; ++i) {
+    ids_base[i] = total;
+    int32_t cnt = 0;
+    for (int t = 0; t < NT; ++t) {
+      int tu = t % nt, tv = t / nt;
+      tile_off[(size_t)i * (NT + 1) + t] = cnt;
+      for (int j = 0; j < N; ++j) {
+        const orc_splat_t *s = &sp[(size_t)i * N + j];
+        if (!s->visible) continue;
+        int u0 = s->ulo > tu * T ? s->ulo : tu * T, u1 = s->uhi < tu * T + T - 1 ? s->uhi : tu * T + T - 1;
+        int v0 = s->vlo > tv * T ? s->vlo : tv * T, v1 = s->vhi < tv * T + T - 1 ? s->vhi : tv * T + T - 1;
+        int keep = 0;
+        for (int v = v0; v <= v1 && !keep; ++v)
+          for (int u = u0; u <= u1 && !keep; ++u) {
+            double dx = ((double)u - half) * px - s->mx, dy = ((double)v - half) * px - s->my;
+            keep = pix_keep(s, s->a * dx * dx + 2.0 * s->b * dx * dy + s->c * dy * dy, pixmask, k, tau);
+          }
+        if (keep) {
+          if (total + cnt >= cap) { free(sp); free(g); return -1; }
+          ids[total + cnt] = j;
+          ++cnt;
+        }
+      }
+    }
+    tile_off[(size_t)i * (NT + 1) + NT] = cnt;
+    total += cnt;
+  }
+  free(sp);
+  free(g);
+  return total;
+}
+
 /* ------------------------------------------------------------------ O5 ---
  * Projection, Eq. 6 with the Eq. 8 selection as contracted:
  *   masked:   I(u,v) = sum_{j visible, (u,v) in AABB_ij} amp exp(-Q/2)

@@ -357,3 +357,46 @@ def test_pixel_mask_variants_closed_form(orc):
     near = np.abs(Q - k * k) < 1e-9
     assert not near.any()
     assert np.array_equal(img != 0, Q <= k * k)
+
+
+def test_lists_pixmask_brute_force(orc):
+    """O4m (f1, exact ellipse-tile intersection): a tile lists j iff one of its pixels inside the
+    AABB has Q <= k^2, checked against a pure-Python scan with Q from numpy's inverse of the
+    projected covariance; the result is a subset of the AABB lists (O4)."""
+    rng = np.random.default_rng(21)
+    N, B, D, T, px, k = 40, 2, 32, 8, 1.0, 3.0
+    params = _random_case(rng, N, D, px, sig_px=(0.6, 3.0), spread=0.6)
+    R = np.stack([Rotation.random(random_state=80 + s).as_matrix() for s in range(B)])
+    sh = rng.uniform(-3, 3, (B, 2))
+    aabb, vis, _ = orc.splats(params, R.reshape(B, 9), sh, D, px, k=k)
+    off, base, ids = orc.lists_pixmask(params, R.reshape(B, 9), sh, D, px, T, 2, k=k)
+    off0, base0, ids0 = orc.lists(aabb, vis, D, T)
+    nt = D // T
+    fewer = 0
+    for i in range(B):
+        W = R[i].T
+        for t in range(nt * nt):
+            tu, tv = t % nt, t // nt
+            exp = []
+            for j in range(N):
+                if not vis[i, j]:
+                    continue
+                Sig = sigma_ref(params[2][j], params[1][j, :3])
+                S2 = (W @ Sig @ W.T)[:2, :2]
+                m = (W @ params[0][j, :3])[:2] + sh[i]
+                Si = np.linalg.inv(S2)
+                u0, u1 = max(aabb[i, j, 0], tu * T), min(aabb[i, j, 1], tu * T + T - 1)
+                v0, v1 = max(aabb[i, j, 2], tv * T), min(aabb[i, j, 3], tv * T + T - 1)
+                hit = False
+                for v in range(v0, v1 + 1):
+                    for u in range(u0, u1 + 1):
+                        x = np.array([(u - D // 2) * px, (v - D // 2) * px]) - m
+                        hit |= x @ Si @ x <= k * k
+                if hit:
+                    exp.append(j)
+            got = ids[base[i] + off[i, t]: base[i] + off[i, t + 1]]
+            assert list(got) == exp, (i, t)
+            full = ids0[base0[i] + off0[i, t]: base0[i] + off0[i, t + 1]]
+            assert set(got) <= set(full)
+            fewer += len(full) - len(got)
+    assert fewer > 0   # some AABB-corner tiles hold no ellipse pixel
