@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--pixel-mask", default="aabb", choices=["aabb", "ellipse", "tau", "ellipse+tau"],
                     help="Eq. 8 per-pixel selection variant (GEM_FLAG_ELLIPSE / GEM_FLAG_PIXEL_TAU)")
     ap.add_argument("--tau", type=float, default=0.0)
+    ap.add_argument("--exact-tiles", action="store_true", help="with --pixel-mask: lists of tiles with a kept pixel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kernel-events", action="store_true",
@@ -239,7 +240,7 @@ def main():
     phantom = gem.SoA.from_arrays(*synth.f32(*synth.phantom(w, synth.seed_for(w.name, "phantom", 0))), dev)
     cfg = gem.GemConfig(D=w.D, pixel_size=px, n_gauss=w.N, max_batch=B, tile=args.tile,
                         lr_mean=1e-3 * w.ball_radius, fused=args.fused, wave=args.wave, zsort=args.zsort,
-                        pixel_mask=args.pixel_mask, tau=args.tau)
+                        pixel_mask=args.pixel_mask, tau=args.tau, exact_tiles=args.exact_tiles)
 
     # device-resident ring of distinct synthetic particles (per-rank seeds)
     rot_np, sh_np, ctf_np = synth.f32(*synth.particles(w, ring, 1000 + rank))
@@ -388,6 +389,7 @@ def main():
         "config": {"workload": f"{w.name}: EMPIAR-10028-shaped, N={w.N} Gaussians, D={w.D}, px={w.px} A",
                    "model_state": args.state, "batch_per_gpu": B, "global_batch": B * world, "tile": args.tile,
                    "fused_waves": args.fused, "wave": int(st["wave"]), "zsort": args.zsort, "pixel_mask": args.pixel_mask, "tau": args.tau,
+                   "exact_tiles": args.exact_tiles,
                    "ring_particles_per_gpu": ring, "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2: per-step working set (splat records "
                          f"{B * w.N * 32 / 1e6:.0f} MB + images) and a {ring}-particle ring "

@@ -108,10 +108,12 @@ typedef struct {
  * must lie in the AABB (as always) and in addition:
  * GEM_FLAG_ELLIPSE      inside the k-sigma ellipse, Q <= cull_k^2 (not only its bounding box);
  * GEM_FLAG_PIXEL_TAU    |amp_ij| exp(-Q/2) >= tau at the pixel.
- * Both apply to the forward and, with the same masks, to the backward.  The tile lists stay
- * AABB-based (a superset).  DESIGN.md §3 L26. */
+ * Both apply to the forward and, with the same masks, to the backward.  DESIGN.md §3 L26.
+ * GEM_FLAG_EXACT_TILES  (with ELLIPSE and/or PIXEL_TAU) a tile lists a Gaussian only if one of
+ *                       its pixels is kept (exact ellipse-tile intersection);
+ *                       without it the lists stay AABB-based (a superset, rendering zeros). */
 enum { GEM_FLAG_FUSED = 1, GEM_FLAG_NO_ROTATION = 2, GEM_FLAG_ISOTROPIC = 4, GEM_FLAG_ZSORT = 8,
-       GEM_FLAG_ELLIPSE = 16, GEM_FLAG_PIXEL_TAU = 32 };
+       GEM_FLAG_ELLIPSE = 16, GEM_FLAG_PIXEL_TAU = 32, GEM_FLAG_EXACT_TILES = 64 };
 
 /* Gaussian parameter store (a0): three float4 arrays of length N.
  *   mean_rho [N] = (mu_x, mu_y, mu_z [Angstrom], rho)

@@ -21,6 +21,7 @@ GEM_FLAG_ISOTROPIC = 4     # Table 5 ablation: tied log-scales
 GEM_FLAG_ZSORT = 8         # P:227 z-sorted per-tile lists
 GEM_FLAG_ELLIPSE = 16      # per-pixel: inside the k-sigma ellipse
 GEM_FLAG_PIXEL_TAU = 32    # per-pixel: |G| >= tau (Eq. 8)
+GEM_FLAG_EXACT_TILES = 64  # lists: only tiles holding a kept pixel
 
 
 class GemConfigC(ctypes.Structure):

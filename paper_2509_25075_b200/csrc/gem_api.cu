@@ -40,7 +40,8 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   d.tau = c.tau;
   d.flags = c.flags;
   if (c.flags & ~(uint32_t)(GEM_FLAG_FUSED | GEM_FLAG_NO_ROTATION | GEM_FLAG_ISOTROPIC | GEM_FLAG_ZSORT |
-                             GEM_FLAG_ELLIPSE | GEM_FLAG_PIXEL_TAU)) return false;
+                             GEM_FLAG_ELLIPSE | GEM_FLAG_PIXEL_TAU | GEM_FLAG_EXACT_TILES)) return false;
+  if ((c.flags & GEM_FLAG_EXACT_TILES) && !(c.flags & (GEM_FLAG_ELLIPSE | GEM_FLAG_PIXEL_TAU))) return false;
   if (c.flags & GEM_FLAG_FUSED) {
     if (c.wave <= 0) {   // auto: keep one wave's splat records, lists and images within ~64 MB of L2
       const double per = (double)d.N * (32 + 8 + 4 * (c.tile == 16 ? 2 : 3)) + (double)c.D * c.D * 4 * 3 +
@@ -409,7 +410,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
                      at<int>(ctx, L.ticket) + 8, st, c.cap, s, ctx->launches);
     }
     uint2 *zpair = (c.flags & GEM_FLAG_ZSORT) ? at<uint2>(ctx, L.zs_key) : nullptr;
-    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<int>(ctx, L.subcnt), ids, (const float4 *)params->mean_rho, rw, zpair, s, ctx->launches); }
+    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<int>(ctx, L.subcnt), ids, (const float4 *)params->mean_rho, rw, zpair, rec, s, ctx->launches); }
     if (zpair) {
       Prof p(ctx, s, P_ZSORT);
       launch_zsort(c, nb, base, (const float4 *)params->mean_rho, rw, ids, zpair, at<int>(ctx, L.zs_tmp),

@@ -109,6 +109,37 @@ enum ProfKind { P_PREP, P_SPLAT, P_SCAN, P_FILL, P_RENDER_FWD, P_FFT_R2C, P_CTF_
                 P_BWD_REDUCE, P_FINALIZE, P_ADAM, P_VOLUME, P_ZSORT, P_COUNT };
 }
 
+// ------------------------------------------- per-pixel selection tile test (GEM_FLAG_ELLIPSE/_PIXEL_TAU)
+namespace gem {
+// Q threshold of the per-pixel selection: a pixel is kept iff Q <= t,
+// t = min(ELLIPSE ? k^2 : inf, PIXEL_TAU ? 2 ln(|amp| / tau) : inf)   (reading L26)
+__device__ __forceinline__ float keep_q(const CfgDev &c, float amp) {
+  float t = (c.flags & GEM_FLAG_ELLIPSE) ? c.k * c.k : 3.0e38f;
+  if ((c.flags & GEM_FLAG_PIXEL_TAU) && c.tau > 0.f) t = fminf(t, 2.f * logf(fabsf(amp) / c.tau));
+  return t;
+}
+// Exact ellipse-tile intersection for the lists: does the pixel block
+// [c0, c1] x [r0, r1] (absolute indices, inside the AABB) hold a pixel with Q <= t?  Row by row
+// the kept columns are u in [ucen + (-b dy - sqrt(disc)) / a, ucen + (-b dy + sqrt(disc)) / a],
+// disc = a t - det dy^2.  Round-to-nearest intrinsics only (no contraction): the splat kernel
+// (histogram) and the fill (ids) call this with the same inputs and must decide identically.
+__device__ __forceinline__ bool tile_kept(float ucen, float vcen, float a, float b, float cc, float t, int c0, int c1,
+                                          int r0, int r1) {
+  const float det = __fsub_rn(__fmul_rn(a, cc), __fmul_rn(b, b));
+  const float at = __fmul_rn(a, t), ia = __frcp_rn(a);
+  for (int v = r0; v <= r1; ++v) {
+    const float dy = __fsub_rn((float)v, vcen);
+    const float disc = __fsub_rn(at, __fmul_rn(det, __fmul_rn(dy, dy)));
+    if (!(disc >= 0.f)) continue;
+    const float sq = __fsqrt_rn(disc), mb = __fmul_rn(-b, dy);
+    const float lo = __fadd_rn(ucen, __fmul_rn(__fsub_rn(mb, sq), ia));
+    const float hi = __fadd_rn(ucen, __fmul_rn(__fadd_rn(mb, sq), ia));
+    if (fmaxf(ceilf(lo), (float)c0) <= fminf(floorf(hi), (float)c1)) return true;
+  }
+  return false;
+}
+}  // namespace gem
+
 // ---------------------------------------------------------------- z-sort keys (GEM_FLAG_ZSORT)
 namespace gem {
 // camera-frame depth of Gaussian j under pose i, ((W20 mx + W21 my) + W22 mz), W = P^T, in fp64
@@ -135,7 +166,7 @@ void launch_scan_1p(const int *in, int *out, int64_t n, unsigned long long *stat
 void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, DevStats *st, int64_t cap, cudaStream_t s,
                  int &launches);
 void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,
-                 const float4 *mean_rho, const float *rot, uint2 *zpair, cudaStream_t s,
+                 const float4 *mean_rho, const float *rot, uint2 *zpair, const SplatRec *rec, cudaStream_t s,
                  int &launches);
 void launch_zsort(const CfgDev &c, int B, const int *base, const float4 *mean_rho, const float *rot, int *ids,
                   const uint2 *zpair, int *tmp, int *queue, cudaStream_t s, int &launches);

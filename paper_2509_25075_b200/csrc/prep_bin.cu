@@ -148,6 +148,7 @@ __device__ __noinline__ bool splat_exact(const GaussPrep &g, const double *W, do
 constexpr int kSplatThreads = 256;
 constexpr int kFillWarps = 4, kSub = kChunk / kFillWarps;   // k_fill warps per chunk, Gaussians per warp
 
+template <bool PM>
 __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, const GaussPrep *__restrict__ prep,
                                                                const float4 *__restrict__ mr,
                                                                const float *__restrict__ rot,
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
   const double px = c.px, half = (double)(c.D / 2), kk = c.k, tau = c.tau, ipx = 1.0 / px;
   const float kf = c.k, ipxf = (float)ipx, px2f = c.px * c.px, Df = (float)c.D, tauf = (float)tau;
   unsigned pairs = 0;
+  constexpr bool pixmask = PM;
   __syncthreads();
   auto emit = [&](int j, bool vis, int ulo, int uhi, int vlo, int vhi, float mxp, float myp, float aa, float bb,
                   float cc2, float ampf) {
@@ -187,8 +189,17 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
       pairs += (unsigned)((uhi - ulo + 1) * (vhi - vlo + 1));
       const int tu0 = (ulo >> c.tshift), tu1 = (uhi >> c.tshift), tv0 = (vlo >> c.tshift), tv1 = (vhi >> c.tshift);
       int *sub = shist + ((j - ch * kChunk) / kSub) * c.NT;
-      for (int tv = tv0; tv <= tv1; ++tv)
-        for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&sub[tv * c.nt + tu], 1);
+      if (!pixmask) {
+        for (int tv = tv0; tv <= tv1; ++tv)
+          for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&sub[tv * c.nt + tu], 1);
+      } else {   // per-pixel selection: only tiles holding a kept pixel (exact ellipse-tile test)
+        const float tq = keep_q(c, ampf), ucen = (float)ulo + mxp, vcen = (float)vlo + myp;
+        for (int tv = tv0; tv <= tv1; ++tv)
+          for (int tu = tu0; tu <= tu1; ++tu)
+            if (tile_kept(ucen, vcen, aa, bb, cc2, tq, max(ulo, tu << c.tshift), min(uhi, (tu << c.tshift) + c.T - 1),
+                          max(vlo, tv << c.tshift), min(vhi, (tv << c.tshift) + c.T - 1)))
+              atomicAdd(&sub[tv * c.nt + tu], 1);
+      }
     } else {
       ulo = 1; uhi = 0; vlo = 1; vhi = 0;
       o.f0 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -448,12 +459,13 @@ __global__ void __launch_bounds__(k1pThreads) k_scan_1p(const int *__restrict__ 
 // zpair[slot] instead of ids[slot] -- one 8-byte store costs the same DRAM sectors as the 4-byte
 // id -- with the key computed once per Gaussian from a coalesced read of mean_rho; the sort
 // kernel reads the pairs and writes the sorted ids.
-template <bool ZK>
+template <bool ZK, bool PM>
 __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 *__restrict__ box,
                                                           const int *__restrict__ base,
                                                           const int *__restrict__ subcnt, int *__restrict__ ids,
                                                           const float4 *__restrict__ mean_rho,
-                                                          const float *__restrict__ rot, uint2 *__restrict__ zpair) {
+                                                          const float *__restrict__ rot, uint2 *__restrict__ zpair,
+                                                          const SplatRec *__restrict__ rec) {
   extern __shared__ int cnt[];   // [kFillWarps][NT] cursors
   const int i = blockIdx.y, ch = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int *mine = cnt + w * c.NT;
@@ -471,6 +483,7 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
     }
   }
   __syncthreads();
+  constexpr bool pixmask = PM;
   const unsigned lt = (1u << lane) - 1u;
   double w0 = 0.0, w1 = 0.0, w2 = 0.0;
   if (ZK) { w0 = (double)rot[9 * i + 2]; w1 = (double)rot[9 * i + 5]; w2 = (double)rot[9 * i + 8]; }
@@ -489,13 +502,27 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
     }
     unsigned key = 0;
     if (ZK && ntu > 0) key = ord32(__double2float_rn(zdepth64(__ldg(mean_rho + j), w0, w1, w2)));
+    // per-pixel selection: the same exact tile test as the splat kernel's histogram
+    float ucen = 0.f, vcen = 0.f, ca = 0.f, cb = 0.f, cc = 0.f, tq = 0.f;
+    int ulo = 0, uhi = -1, vlo = 0, vhi = -1;
+    if (pixmask && ntu > 0) {
+      const SplatRec r = rec[(size_t)i * c.N + j];
+      ulo = (int)(__float_as_uint(r.f1.z) & 0xffff); uhi = (int)(__float_as_uint(r.f1.z) >> 16);
+      vlo = (int)(__float_as_uint(r.f1.w) & 0xffff); vhi = (int)(__float_as_uint(r.f1.w) >> 16);
+      ucen = (float)ulo + r.f0.x; vcen = (float)vlo + r.f0.y;
+      ca = r.f0.z; cb = r.f0.w; cc = r.f1.x; tq = keep_q(c, r.f1.y);
+    }
     // slot-major order: every lane's tile (dv, du) of its rectangle, (dv, du) ascending, then lane
     const int mu = __reduce_max_sync(0xffffffffu, (unsigned)max(ntu, 0));
     const int mv = __reduce_max_sync(0xffffffffu, (unsigned)ntv);
     for (int dv = 0; dv < mv; ++dv) {
       for (int du = 0; du < mu; ++du) {
-        const bool active = du < ntu && dv < ntv;
-        const int t = (tv0 + dv) * c.nt + tu0 + du;
+        const int tu = tu0 + du, tv = tv0 + dv;
+        const bool active = du < ntu && dv < ntv &&
+                            (!pixmask || tile_kept(ucen, vcen, ca, cb, cc, tq, max(ulo, tu << c.tshift),
+                                                   min(uhi, (tu << c.tshift) + c.T - 1), max(vlo, tv << c.tshift),
+                                                   min(vhi, (tv << c.tshift) + c.T - 1)));
+        const int t = tv * c.nt + tu;
         const unsigned m = __match_any_sync(0xffffffffu, active ? t : -1);
         const int rank = __popc(m & lt);
         if (active) {
@@ -528,10 +555,14 @@ void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const flo
   const size_t smem = (kFillWarps * c.NT + kChunk) * sizeof(int);
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(k_splat_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_splat_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_splat_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     init = true;
   }
-  k_splat_count<<<grid, kSplatThreads, smem, s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, subcnt, st);
+  if (c.flags & GEM_FLAG_EXACT_TILES)
+    k_splat_count<true><<<grid, kSplatThreads, smem, s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, subcnt, st);
+  else
+    k_splat_count<false><<<grid, kSplatThreads, smem, s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, subcnt, st);
   ++launches;
 }
 
@@ -550,17 +581,14 @@ void launch_scan_1p(const int *in, int *out, int64_t n, unsigned long long *stat
 }
 
 void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,
-                 const float4 *mean_rho, const float *rot, uint2 *zpair, cudaStream_t s, int &launches) {
+                 const float4 *mean_rho, const float *rot, uint2 *zpair, const SplatRec *rec, cudaStream_t s,
+                 int &launches) {
   dim3 grid(c.C, B);
   const size_t smem = (size_t)kFillWarps * c.NT * sizeof(int);
-  if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(k_fill<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_fill<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
-  if (zpair)
-    k_fill<true><<<grid, kFillWarps * 32, smem, s>>>(c, box, base, subcnt, ids, mean_rho, rot, zpair);
-  else
-    k_fill<false><<<grid, kFillWarps * 32, smem, s>>>(c, box, base, subcnt, ids, mean_rho, rot, zpair);
+  const bool pm = (c.flags & GEM_FLAG_EXACT_TILES) != 0;
+  auto kern = zpair ? (pm ? k_fill<true, true> : k_fill<true, false>) : (pm ? k_fill<false, true> : k_fill<false, false>);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, kFillWarps * 32, smem, s>>>(c, box, base, subcnt, ids, mean_rho, rot, zpair, rec);
   ++launches;
 }
 

@@ -37,6 +37,7 @@ class GemConfig:
     ablation: str = "full"   # Table 5: full | no_rotation | isotropic_scale | both
     zsort: bool = False      # P:227 z-sorted per-tile lists (GEM_FLAG_ZSORT)
     pixel_mask: str = "aabb"  # Eq. 8 per-pixel selection: aabb | ellipse | tau | ellipse+tau
+    exact_tiles: bool = False  # with a pixel mask: lists hold only tiles with a kept pixel
 
     def c(self) -> _b.GemConfigC:
         return _b.GemConfigC(self.D, self.pixel_size, self.n_gauss, self.max_batch, self.cull_k, self.tau, self.tile,
@@ -55,6 +56,8 @@ class GemConfig:
             f |= _b.GEM_FLAG_ELLIPSE
         if "tau" in self.pixel_mask:
             f |= _b.GEM_FLAG_PIXEL_TAU
+        if self.exact_tiles:
+            f |= _b.GEM_FLAG_EXACT_TILES
         if self.ablation in ("no_rotation", "both"):
             f |= _b.GEM_FLAG_NO_ROTATION
         if self.ablation in ("isotropic_scale", "both"):

@@ -81,9 +81,9 @@ def maxnorm_rel(a, b):
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
 
 
-def assert_lists_exact(orc, case, lists, tile, first=0):
+def assert_lists_exact(orc, case, lists, tile, first=0, tau=0.0):
     w = case["w"]
-    aabb, vis, sp = orc.splats(case["params"], case["rot"], case["shift"], w.D, case["px"])
+    aabb, vis, sp = orc.splats(case["params"], case["rot"], case["shift"], w.D, case["px"], tau=tau)
     tile_off, base, ids = orc.lists(aabb, vis, w.D, tile)
     ties = 0
     for ii, (g_off, g_ids, g_box) in enumerate(lists):
@@ -473,8 +473,9 @@ def mask_ties(orc, case, pixmask, tau, k=3.0, band=1e-4):
     return n
 
 
-@pytest.mark.parametrize("variant", ["ellipse", "tau", "ellipse+tau"])
-def test_pixel_mask_variants(gem, orc, variant):
+@pytest.mark.parametrize("variant,exact", [("ellipse", False), ("tau", False), ("ellipse+tau", False),
+                                           ("ellipse", True), ("ellipse+tau", True)])
+def test_pixel_mask_variants(gem, orc, variant, exact):
     """f1: per-pixel selection (exact k-sigma ellipse, per-pixel tau of Eq. 8) on the GPU against
     the oracle (masks applied in forward and backward).  Cases are chosen with no pixel within
     1e-4 (in Q) of a mask boundary, where fp32 and fp64 could decide differently (the GPU's
@@ -488,7 +489,8 @@ def test_pixel_mask_variants(gem, orc, variant):
     else:
         pytest.fail("no tie-free case")
     w = case["w"]
-    cfg = gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=3, tau=tau, pixel_mask=variant)
+    cfg = gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=3, tau=tau, pixel_mask=variant,
+                        exact_tiles=exact)
     st = gem.GemStep(cfg)
     dev = st.device
     P = gem.SoA.from_arrays(*case["params"], device=dev)
@@ -511,6 +513,22 @@ def test_pixel_mask_variants(gem, orc, variant):
     assert np.all(np.abs(lo[:-1] - o["loss"]) < LOSS_TOL * o["loss"])
     for name, cols in CLASSES.items():
         assert maxnorm_rel(g[:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+    if not exact:
+        assert_lists_exact(orc, case, [st.export_lists(i) for i in range(3)], 8, tau=tau)   # AABB lists
+        return
+    # exact ellipse-tile intersection: the lists hold exactly the tiles with a kept pixel (O4m)
+    off, base, ids = orc.lists_pixmask(case["params"], case["rot"], case["shift"], w.D, case["px"], 8, pm, tau=tau)
+    pruned = 0
+    for i in range(3):
+        g_off, g_ids, _ = st.export_lists(i)
+        assert np.array_equal(g_off, off[i]), i
+        o_ids = ids[base[i]: base[i] + off[i, -1]]
+        for t in range(len(g_off) - 1):
+            assert np.array_equal(np.sort(g_ids[g_off[t]:g_off[t + 1]]), o_ids[off[i, t]:off[i, t + 1]]), (i, t)
+        aabb, vis, _ = orc.splats(case["params"], case["rot"][i:i + 1], case["shift"][i:i + 1], w.D, case["px"],
+                                  tau=tau)
+        pruned += orc.lists(aabb, vis, w.D, 8)[0][0, -1] - g_off[-1]
+    assert pruned > 0   # AABB-corner tiles without a kept pixel are gone
 
 
 def test_X_config_sampled(gem, orc):
