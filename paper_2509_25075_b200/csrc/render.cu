@@ -30,8 +30,9 @@ __device__ __forceinline__ float ex2(float x) {
 // columns and r rows from the box corner carries ~(k^2 + r^2)/4 ulp relative to its own value.
 // Safety: f <= 0, so values never overflow; the recurrences stay exact only while their factors
 // are normal numbers, so an entry whose first-column values fall below 2^-100 amp (needle-like
-// Gaussians at far AABB corners), whose corner row ratio is below 2^-120, whose W, Kb leave the
-// normal range, or whose amplitude is negative is evaluated directly (exp per pixel).
+// Gaussians at far AABB corners), whose corner row ratio is below 2^-120, or whose W, Kb leave the
+// normal range is evaluated directly (exp per pixel).  The amplitude's sign only multiplies
+// (negative densities take the fast path too).
 constexpr int kFwdWarps = 2;       // warps per CTA (independent)
 constexpr int kCH = 64;            // list entries staged per chunk per warp
 
@@ -157,11 +158,11 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
         const float dx0 = (float)cu0 - mx;
         const float Fx = na * dx0 * dx0, Gx = nb2 * dx0, D0 = na * fmaf(2.f, dx0, 1.f);
         // the recurrence needs its factors normal: first-column values and the row ratio at the
-        // covered rows (f concave, ratio linear in dy: check the end rows) and the amplitude sign
+        // covered rows (f concave, ratio linear in dy: check the end rows)
         const float d0 = (float)cv0 - my, d1 = (float)cv1 - my;
         const float f0 = fmaf(d0, fmaf(nc, d0, Gx), Fx), f1 = fmaf(d1, fmaf(nc, d1, Gx), Fx);
         const float r0 = fmaf(nb2, d0, D0), r1 = fmaf(nb2, d1, D0);
-        const bool slow = !(fminf(f0, f1) >= -100.f && fminf(r0, r1) >= -120.f && rr.f1.y > 0.f);
+        const bool slow = !(fminf(f0, f1) >= -100.f && fminf(r0, r1) >= -120.f);
         sm.eA[qc] = make_float4(my, nb2, nc, rr.f1.y);
         sm.eB[qc] = make_float4(Fx, Gx, D0, ex2(2.f * na));
         sm.eC[qc] = make_float2(na, __int_as_float(cu0 | (cu1 << 8) | (cv0 << 16) | (cv1 << 24) |
@@ -200,8 +201,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
           for (int k = 0; k < T; ++k) {
             if (k >= k0 && k <= k1) {
               if (MK) {
-                acc[k].x += E2.x >= th ? E2.x : 0.f;
-                acc[k].y += E2.y >= th ? E2.y : 0.f;
+                acc[k].x += fabsf(E2.x) >= th ? E2.x : 0.f;
+                acc[k].y += fabsf(E2.y) >= th ? E2.y : 0.f;
               } else {
                 acc[k] = __fadd2_rn(acc[k], E2);
               }
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
       const float gS = fmaf(nb2, dyS, D0), gE = fmaf(nb2, dyE, D0);
       const float hS = fmaf(nc, fmaf(2.f, dyS, 1.f), Gx), hE = fmaf(nc, fmaf(2.f, dyE, 1.f), Gx);
       const bool slow = !(fminf(fS, fE) >= -100.f && fminf(gS, gE) >= -120.f && fmaxf(fabsf(hS), fabsf(hE)) <= 60.f &&
-                          nc >= -30.f && fabsf(nb2) <= 60.f && amp > 0.f);
+                          nc >= -30.f && fabsf(nb2) <= 60.f);
       const float th = MK ? keep_thr(c, amp, eK) : 0.f;
       if (!slow) {
         const float EA = amp * ex2(fS), VA = ex2(hS), RA = ex2(gS);
@@ -364,8 +365,8 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
           for (int k = 0; k < T; ++k) {
             if (cm & (1u << k)) {
               if (MK) {
-                acc[p][k].x += Em.x >= th ? Em.x : 0.f;
-                acc[p][k].y += Em.y >= th ? Em.y : 0.f;
+                acc[p][k].x += fabsf(Em.x) >= th ? Em.x : 0.f;
+                acc[p][k].y += fabsf(Em.y) >= th ? Em.y : 0.f;
               } else {
                 acc[p][k] = __fadd2_rn(acc[p][k], Em);
               }
