@@ -559,3 +559,22 @@ def test_X_config_sampled(gem, orc):
     tot = parts[0] + parts[1]
     for name, cols in CLASSES.items():
         assert maxnorm_rel(g["grad"][:, cols], tot[:, cols]) < 1e-5, name
+
+
+@pytest.mark.parametrize("tile", [8, 16])
+def test_negative_densities(gem, orc, tile):
+    """Training can drive densities negative; those Gaussians take the recurrence (fast) path
+    with a negative amplitude and must match the oracle like positive ones."""
+    case = make_case("T", B=3, seed=23)
+    mr = case["params"][0].copy()
+    rng = np.random.default_rng(2)
+    neg = rng.random(mr.shape[0]) < 0.3
+    mr[neg, 3] *= -1.0
+    case["params"] = (mr, case["params"][1], case["params"][2])
+    g = run_gpu(gem, case, tile=tile, want_lists=True)
+    assert_lists_exact(orc, case, g["lists"], tile)
+    o = oracle_out(orc, case)
+    for i in range(3):
+        assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
+    for name, cols in CLASSES.items():
+        assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
