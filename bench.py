@@ -189,7 +189,7 @@ def run_reference(args, rank, world):
     t1 = oracle_step_sample(w, 1)
     budget = 150.0
     steps = args.steps
-    warm = min(args.warmup, 1)
+    warm = args.warmup
     per_step = 1
     if (steps + warm) * t1 > budget:
         steps = max(1, int(budget // t1) - warm)
