@@ -148,13 +148,18 @@ __global__ void __launch_bounds__(128) k_loss_reduce(int B, int nblk, const doub
 
 }  // namespace
 
-void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
+void launch_ctf_params(const CfgDev &c, int B, const float *ctf, void *ctf_par, cudaStream_t s, int &launches) {
+  k_ctf_params<<<(B + 127) / 128, 128, 0, s>>>(B, 1.0 / ((double)c.D * (double)c.px), ctf,
+                                                reinterpret_cast<CtfP *>(ctf_par));
+  ++launches;
+}
+
+void launch_ctf_loss(const CfgDev &c, int B, const void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
                      float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches) {
-  CtfP *P = reinterpret_cast<CtfP *>(ctf_par);
-  k_ctf_params<<<(B + 127) / 128, 128, 0, s>>>(B, 1.0 / ((double)c.D * (double)c.px), ctf, P);
   dim3 grid(loss_blocks, B);
-  k_ctf_loss<<<grid, kCtfThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part);
-  launches += 2;
+  k_ctf_loss<<<grid, kCtfThreads, 0, s>>>(c, reinterpret_cast<const CtfP *>(ctf_par), spec_hat, spec_obs, spec_pred,
+                                           loss_part);
+  ++launches;
 }
 
 void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, int *ticket,

@@ -267,7 +267,9 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
   ctx->fused = (c.flags & GEM_FLAG_FUSED) ? 1 : 0;
   if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_ctf, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_loss, cudaEventDisableTiming) != cudaSuccess) {
     delete ctx;
     return GEM_E_CUDA;
   }
@@ -299,6 +301,8 @@ gem_status gem_destroy(gem_ctx *ctx) {
     cudaStreamDestroy(ctx->side);
     cudaEventDestroy(ctx->ev_fork);
     cudaEventDestroy(ctx->ev_join);
+    cudaEventDestroy(ctx->ev_ctf);
+    cudaEventDestroy(ctx->ev_loss);
   }
   for (int k = 0; k < 2 * ctx->prof_cap; ++k) cudaEventDestroy(ctx->prof_ev[k]);
   free(ctx->prof_ev);
@@ -389,8 +393,9 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     cufftHandle r2c, c2r, r2c_obs;
     gem_status ps = plan_for(ctx, nb, &r2c, &c2r, &r2c_obs);
     if (ps != GEM_OK) return ps;
-    // fork: the observed images' R2C runs on the internal side stream, overlapped with the
-    // splat / binning / render of this wave; joined before the CTF/loss kernel
+    // fork: the observed images' R2C and the per-particle CTF constants run on the internal side
+    // stream, overlapped with the splat / binning / render of this wave; joined before the
+    // CTF/loss kernel
     CK(cudaEventRecord(ctx->ev_fork, s));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     CKF(cufftSetStream(r2c_obs, ctx->side));
@@ -398,6 +403,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
       Prof p(ctx, ctx->side, P_FFT_OBS);
       CKF(cufftExecR2C(r2c_obs, (cufftReal *)(obs + p0 * DD), (cufftComplex *)so));
     }
+    { Prof p(ctx, ctx->side, P_CTF_LOSS); launch_ctf_params(c, nb, ctf + 8 * (size_t)p0, ctx->ws + L.ctf_par, ctx->side, ctx->launches); }
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
     const float *rw = rot + 9 * (size_t)p0;
     { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist, at<int>(ctx, L.subcnt), st, s,
@@ -427,9 +433,10 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     {
       Prof p(ctx, s, P_CTF_LOSS);
-      launch_ctf_loss(c, nb, ctf + 8 * (size_t)p0, ctx->ws + L.ctf_par, sh, so, pred_out ? sp : nullptr, lpart + (size_t)p0 * L.loss_blocks,
+      launch_ctf_loss(c, nb, ctx->ws + L.ctf_par, sh, so, pred_out ? sp : nullptr, lpart + (size_t)p0 * L.loss_blocks,
                       L.loss_blocks, s, ctx->launches);
     }
+    CK(cudaEventRecord(ctx->ev_ctf, s));
     {
       Prof p(ctx, s, P_FFT_C2R);
       if (pred_out) CKF(cufftExecC2R(c2r, (cufftComplex *)sp, (cufftReal *)(pred_out + p0 * DD)));
@@ -447,9 +454,14 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
   }
   ctx->last_p0 = p0 - ctx->W;
   ctx->last_nb = nb;
+  // the per-particle loss reduction (and the host copy of the loss) runs on the side stream,
+  // overlapped with the last C2R; the caller's stream joins it before anything that follows
   double *lossd = host ? at<double>(ctx, L.stage_loss) : loss;
-  { Prof p(ctx, s, P_CTF_LOSS); launch_loss_reduce(B, lpart, L.loss_blocks, lossd, st, at<int>(ctx, L.ticket) + 4, s, ctx->launches); }
-  if (host) CK(cudaMemcpyAsync(loss, lossd, sizeof(double) * (B + 1), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_ctf, 0));
+  { Prof p(ctx, ctx->side, P_CTF_LOSS); launch_loss_reduce(B, lpart, L.loss_blocks, lossd, st, at<int>(ctx, L.ticket) + 4, ctx->side, ctx->launches); }
+  if (host) CK(cudaMemcpyAsync(loss, lossd, sizeof(double) * (B + 1), cudaMemcpyDeviceToHost, ctx->side));
+  CK(cudaEventRecord(ctx->ev_loss, ctx->side));
+  CK(cudaStreamWaitEvent(s, ctx->ev_loss, 0));
   CK(cudaGetLastError());
   ctx->fwd_live = 1;
   ctx->last_B = B;

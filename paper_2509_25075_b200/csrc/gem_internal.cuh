@@ -88,7 +88,7 @@ struct gem_ctx {
   int plan_B[8];
   cufftHandle plan_r2c[8], plan_c2r[8], plan_obs[8];   // plan_obs: R2C of the observed images (side stream)
   cudaStream_t side;   // internal stream: observed-image R2C overlapped with splat/bin/render
-  cudaEvent_t ev_fork, ev_join;
+  cudaEvent_t ev_fork, ev_join, ev_ctf, ev_loss;   // side-stream fork / join points
   int n_plans;
   int fwd_live;        // a forward's lists/records/dL/dI are valid
   int last_B;
@@ -172,7 +172,8 @@ void launch_zsort(const CfgDev &c, int B, const int *base, const float4 *mean_rh
                   const uint2 *zpair, int *tmp, int *queue, cudaStream_t s, int &launches);
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
                        int *ticket, cudaStream_t s, int &launches);
-void launch_ctf_loss(const CfgDev &c, int B, const float *ctf, void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
+void launch_ctf_params(const CfgDev &c, int B, const float *ctf, void *ctf_par, cudaStream_t s, int &launches);
+void launch_ctf_loss(const CfgDev &c, int B, const void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
                      float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches);
 size_t ctf_par_bytes();
 void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, int *ticket,
