@@ -52,7 +52,7 @@ __device__ __forceinline__ void retire(int *ticket, int lane) {
   }
 }
 
-// Forward kernel.  Register accumulators: lane L owns row pair p = L / NCP of the tile
+// Forward kernel for 16 x 16 tiles (8 x 8 tiles use k_render_fwd_le below).  Register accumulators: lane L owns row pair p = L / NCP of the tile
 // (NCP = 32 / NP lanes per pair) and keeps a private copy of that pair-row, T columns x 2 rows,
 // in registers.  Per chunk of <= kCH entries, each lane takes one entry (records prefetched one
 // 32-entry group ahead, ids two), stores its per-entry constants once in shared memory and
@@ -654,12 +654,9 @@ void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *b
                    : persistent_grid(k_render_fwd_le<false>, kLeWarps * 32, 0);
     if (mk) k_render_fwd_le<true><<<g, kLeWarps * 32, 0, s>>>(c, B, rec, base, ids, proj, ticket);
     else k_render_fwd_le<false><<<g, kLeWarps * 32, 0, s>>>(c, B, rec, base, ids, proj, ticket);
-  } else if (c.T == 16) {
+  } else {   // 16 x 16 tiles: lanes own row pairs, entries binned per pair (k_render_fwd<16>)
     if (mk) launch_fwd_t<16, true>(c, B, rec, base, ids, proj, ticket, s);
     else launch_fwd_t<16, false>(c, B, rec, base, ids, proj, ticket, s);
-  } else {
-    if (mk) launch_fwd_t<8, true>(c, B, rec, base, ids, proj, ticket, s);
-    else launch_fwd_t<8, false>(c, B, rec, base, ids, proj, ticket, s);
   }
   ++launches;
 }
