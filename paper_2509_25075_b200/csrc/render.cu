@@ -52,8 +52,9 @@ __device__ __forceinline__ void retire(int *ticket, int lane) {
   }
 }
 
-// Forward kernel for 16 x 16 tiles (8 x 8 tiles use k_render_fwd_le below).  Register accumulators: lane L owns row pair p = L / NCP of the tile
-// (NCP = 32 / NP lanes per pair) and keeps a private copy of that pair-row, T columns x 2 rows,
+// Forward kernel for 16 x 16 tiles (8 x 8 tiles use k_render_fwd_le below).  Register
+// accumulators: lane L owns row pair p = L / NCP of the tile (NCP = 32 / NP lanes per pair)
+// and keeps a private copy of that pair-row, T columns x 2 rows,
 // in registers.  Per chunk of <= kCH entries, each lane takes one entry (records prefetched one
 // 32-entry group ahead, ids two), stores its per-entry constants once in shared memory and
 // appends the entry's index to the bin of every row pair its box covers (ballots, in list
