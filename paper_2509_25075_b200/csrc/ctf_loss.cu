@@ -146,6 +146,178 @@ __global__ void __launch_bounds__(128) k_loss_reduce(int B, int nblk, const doub
   }
 }
 
+// ------------------------------------------------------------- row-column spectral path
+// For D = R1 R2 in {32, 64, 128, 256} the 2D transforms are split (DESIGN.md §6 a6): cuFFT does
+// only the row transforms (1D R2C of the projections and the observations, 1D C2R of the
+// gradient), and one kernel does everything along the columns: for each half-spectrum column
+// kx, the forward column FFTs of F(I_hat) and F(I_obs), the CTF / residual / Parseval loss /
+// gradient spectrum per bin, and the inverse column FFT of the gradient spectrum, in place.
+// Row then column = the 2D DFT (separable), so the loss and gradient are those of k_ctf_loss.
+// A group of R2 threads transforms one column (length D, four-step: R1-point DFTs in registers,
+// twiddles, a transpose through shared memory, R2-point DFTs); R1 values per thread.
+// cos and sin of 2 pi j / 16 (the twiddles of the in-register DFTs are compile-time constants)
+__device__ __forceinline__ float c16(int j) {
+  constexpr float v[16] = {1.f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f, 0.f,
+                           -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f, -1.f,
+                           -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f, 0.f,
+                           0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+  return v[j & 15];
+}
+__device__ __forceinline__ float s16(int j) { return c16(j + 12); }   // sin x = cos(x - pi/2)
+
+template <int R>
+__device__ __forceinline__ void dft_reg(float2 (&a)[R]) {
+  // radix-2 decimation in frequency in registers, W_R^j = exp(-2 pi i j / R); natural-order output
+#pragma unroll
+  for (int half = R / 2; half >= 1; half >>= 1) {
+#pragma unroll
+    for (int b = 0; b < R; b += 2 * half) {
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const float2 u = a[b + j], v = a[b + j + half];
+        const int e = j * (16 / (2 * half));   // W_{2 half}^j = W_16^e
+        const float wr = c16(e), wi = -s16(e);
+        const float dx = u.x - v.x, dy = u.y - v.y;
+        a[b + j] = make_float2(u.x + v.x, u.y + v.y);
+        if (e == 0) a[b + j + half] = make_float2(dx, dy);
+        else if (e == 4) a[b + j + half] = make_float2(dy, -dx);   // times -i
+        else a[b + j + half] = make_float2(dx * wr - dy * wi, dx * wi + dy * wr);
+      }
+    }
+  }
+  float2 t[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    int r = 0;
+#pragma unroll
+    for (int bit = 1, rb = R / 2; bit < R; bit <<= 1, rb >>= 1) r |= (k & bit) ? rb : 0;
+    t[k] = a[r];
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) a[k] = t[k];
+}
+
+// forward (unnormalised) DFT of one column held as v[n1] = x[R2 n1 + t]; on return
+// v[s R2 + k2] = X[(t S + s) + R1 k2], S = R1 / R2
+template <int R1, int R2>
+__device__ __forceinline__ void fft_col(float2 (&v)[R1], int t, float2 *sb, const float2 *__restrict__ tw) {
+  constexpr int S = R1 / R2, P = R2 + 1;   // padded pitch: the transposed reads are conflict-free
+  dft_reg<R1>(v);
+  const float2 w1 = tw[t];   // W_D^(t k1) by recurrence (no bank-conflicting table lookups)
+  float2 w = w1;
+#pragma unroll
+  for (int k1 = 1; k1 < R1; ++k1) {
+    const float2 x = v[k1];
+    v[k1] = make_float2(x.x * w.x - x.y * w.y, x.x * w.y + x.y * w.x);
+    w = make_float2(w.x * w1.x - w.y * w1.y, w.x * w1.y + w.y * w1.x);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) sb[k1 * P + t] = v[k1];
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    float2 u[R2];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) u[n2] = sb[(t * S + s) * P + n2];
+    dft_reg<R2>(u);
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) v[s * R2 + k2] = u[k2];
+  }
+  __syncwarp();
+}
+
+constexpr int kColThreads = 128;
+
+template <int R1, int R2>
+__global__ void __launch_bounds__(kColThreads) k_ctf_colspec(CfgDev c, const CtfP *__restrict__ ctfp,
+                                                             float2 *__restrict__ spec, const float2 *__restrict__ sobs,
+                                                             float2 *__restrict__ spred, double *__restrict__ part) {
+  constexpr int D = R1 * R2, S = R1 / R2, G = kColThreads / R2, Hx = D / 2 + 1;
+  __shared__ float2 tw[D];
+  __shared__ float2 sb[G][R1 * (R2 + 1)];
+  __shared__ double red[kColThreads / 32];
+  for (int j = threadIdx.x; j < D; j += kColThreads) {
+    float sn, cs;
+    sincospif(2.0f * (float)j / (float)D, &sn, &cs);
+    tw[j] = make_float2(cs, -sn);   // W_D^j = exp(-2 pi i j / D)
+  }
+  __syncthreads();
+  const int i = blockIdx.y, g = threadIdx.x / R2, t = threadIdx.x % R2;
+  const int kx0 = blockIdx.x * G + g;
+  const bool act = kx0 < Hx;
+  const int kx = act ? kx0 : Hx - 1;
+  const size_t col = (size_t)i * D * Hx + kx;
+  float2 f[R1], o[R1];
+#pragma unroll
+  for (int n1 = 0; n1 < R1; ++n1) {
+    const size_t r = col + (size_t)(R2 * n1 + t) * Hx;
+    f[n1] = spec[r];
+    o[n1] = sobs[r];
+  }
+  fft_col<R1, R2>(f, t, sb[g], tw);
+  fft_col<R1, R2>(o, t, sb[g], tw);
+  const CtfP P = ctfp[i];
+  const float gsc = 2.0f / ((float)D * (float)D), ps = 1.0f / ((float)D * (float)D);
+  const bool nx = 2 * kx == D;
+  const float wgt = (kx == 0 || nx) ? 1.f : 2.f;
+  const double kxd = kx;
+  float lsum = 0.f;
+#pragma unroll
+  for (int q = 0; q < R1; ++q) {
+    const int ky = (t * S + q / R2) + R1 * (q % R2);
+    const bool ny = 2 * ky == D;
+    const double kyd = 2 * ky < D ? ky : ky - D;
+    // Nyquist bins average their +-1/(2 px) aliases (reading L12): sign flips of kx or ky
+    float C = 0.f;
+    for (int a = 0; a < (nx ? 2 : 1); ++a)
+      for (int b2 = 0; b2 < (ny ? 2 : 1); ++b2) {
+        const double fx = a ? -kxd : kxd, fy = b2 ? -kyd : kyd;
+        C += ctf_raw(P, fx * fx + fy * fy, fx * fx - fy * fy, 2.0 * fx * fy);
+      }
+    if (nx || ny) C *= (nx && ny) ? 0.25f : 0.5f;
+    const float2 F = f[q], Ob = o[q];
+    const float Rr = C * F.x - Ob.x, Ri = C * F.y - Ob.y;
+    lsum = fmaf(wgt, fmaf(Rr, Rr, Ri * Ri), lsum);
+    f[q] = make_float2(gsc * C * Rr, gsc * C * Ri);
+    o[q] = make_float2(C * F.x * ps, C * F.y * ps);
+  }
+  // inverse column DFT (unnormalised) = conj(DFT(conj(.))), back into row-spectrum order
+  auto inverse_store = [&](float2 (&v)[R1], float2 *dst) {
+#pragma unroll
+    for (int q = 0; q < R1; ++q) {
+      const int ky = (t * S + q / R2) + R1 * (q % R2);
+      sb[g][ky] = make_float2(v[q].x, -v[q].y);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) v[n1] = sb[g][R2 * n1 + t];
+    __syncwarp();
+    fft_col<R1, R2>(v, t, sb[g], tw);
+    if (act) {
+#pragma unroll
+      for (int q = 0; q < R1; ++q) {
+        const int row = (t * S + q / R2) + R1 * (q % R2);
+        dst[col + (size_t)row * Hx] = make_float2(v[q].x, -v[q].y);
+      }
+    }
+  };
+  inverse_store(f, spec);
+  if (spred) inverse_store(o, spred);
+  double ls = act ? (double)lsum : 0.0;
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, d);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ls;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < kColThreads / 32; ++w) sum += red[w];
+    part[(size_t)i * gridDim.x + blockIdx.x] = sum / ((double)D * (double)D);
+  }
+}
+
+template <int R1, int R2>
+int colspec_blocks() { return (R1 * R2 / 2 + 1 + kColThreads / R2 - 1) / (kColThreads / R2); }
+
 }  // namespace
 
 void launch_ctf_params(const CfgDev &c, int B, const float *ctf, void *ctf_par, cudaStream_t s, int &launches) {
@@ -154,11 +326,19 @@ void launch_ctf_params(const CfgDev &c, int B, const float *ctf, void *ctf_par, 
   ++launches;
 }
 
+bool spectral_rows(int D) { return D == 32 || D == 64 || D == 128 || D == 256; }
+
 void launch_ctf_loss(const CfgDev &c, int B, const void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
                      float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches) {
+  const CtfP *P = reinterpret_cast<const CtfP *>(ctf_par);
   dim3 grid(loss_blocks, B);
-  k_ctf_loss<<<grid, kCtfThreads, 0, s>>>(c, reinterpret_cast<const CtfP *>(ctf_par), spec_hat, spec_obs, spec_pred,
-                                           loss_part);
+  switch (spectral_rows(c.D) ? c.D : 0) {
+    case 32: k_ctf_colspec<8, 4><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part); break;
+    case 64: k_ctf_colspec<8, 8><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part); break;
+    case 128: k_ctf_colspec<16, 8><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part); break;
+    case 256: k_ctf_colspec<16, 16><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part); break;
+    default: k_ctf_loss<<<grid, kCtfThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part);
+  }
   ++launches;
 }
 
@@ -170,6 +350,14 @@ void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double 
 
 size_t ctf_par_bytes() { return sizeof(CtfP); }
 
-int ctf_loss_blocks(int D) { return (D + kCtfRows - 1) / kCtfRows; }
+int ctf_loss_blocks(int D) {
+  switch (spectral_rows(D) ? D : 0) {
+    case 32: return colspec_blocks<8, 4>();
+    case 64: return colspec_blocks<8, 8>();
+    case 128: return colspec_blocks<16, 8>();
+    case 256: return colspec_blocks<16, 16>();
+    default: return (D + kCtfRows - 1) / kCtfRows;
+  }
+}
 
 }  // namespace gem

@@ -60,11 +60,22 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   return true;
 }
 
+// 2D plans, or -- on the row-column spectral path (spectral_rows(D), see ctf_loss.cu) -- 1D
+// plans over the B*D rows of the batch (R2C: real rows of D -> D/2+1 bins; C2R the reverse)
 bool make_plan(int D, int B, cufftType type, cufftHandle *h, size_t *ws) {
   if (cufftCreate(h) != CUFFT_SUCCESS) return false;
   if (cufftSetAutoAllocation(*h, 0) != CUFFT_SUCCESS) { cufftDestroy(*h); return false; }
-  int n[2] = {D, D};
-  if (cufftMakePlanMany(*h, 2, n, nullptr, 1, 0, nullptr, 1, 0, type, B, ws) != CUFFT_SUCCESS) {
+  cufftResult r;
+  if (spectral_rows(D)) {
+    int n[1] = {D};
+    const int Hx = D / 2 + 1;
+    const bool fwd = type == CUFFT_R2C;
+    r = cufftMakePlanMany(*h, 1, n, n, 1, fwd ? D : Hx, n, 1, fwd ? Hx : D, type, B * D, ws);
+  } else {
+    int n[2] = {D, D};
+    r = cufftMakePlanMany(*h, 2, n, nullptr, 1, 0, nullptr, 1, 0, type, B, ws);
+  }
+  if (r != CUFFT_SUCCESS) {
     cufftDestroy(*h);
     return false;
   }

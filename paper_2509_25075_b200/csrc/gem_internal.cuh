@@ -176,6 +176,7 @@ void launch_ctf_params(const CfgDev &c, int B, const float *ctf, void *ctf_par, 
 void launch_ctf_loss(const CfgDev &c, int B, const void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
                      float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches);
 size_t ctf_par_bytes();
+bool spectral_rows(int D);   // row-column spectral path (1D row plans + column kernel)
 void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, int *ticket,
                         cudaStream_t s,
                         int &launches);
