@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(kColThreads) k_ctf_colspec(CfgDev c, const Ctf
   constexpr int D = R1 * R2, S = R1 / R2, G = kColThreads / R2, Hx = D / 2 + 1;
   __shared__ float2 tw[D];
   __shared__ float2 sb[G][R1 * (R2 + 1)];
+  __shared__ float2 so[R1][kColThreads];   // the observation's column spectrum, off the registers
   __shared__ double red[kColThreads / 32];
   for (int j = threadIdx.x; j < D; j += kColThreads) {
     float sn, cs;
@@ -247,15 +248,18 @@ __global__ void __launch_bounds__(kColThreads) k_ctf_colspec(CfgDev c, const Ctf
   const bool act = kx0 < Hx;
   const int kx = act ? kx0 : Hx - 1;
   const size_t col = (size_t)i * D * Hx + kx;
-  float2 f[R1], o[R1];
+  float2 f[R1];
+  {
+    float2 o[R1];
 #pragma unroll
-  for (int n1 = 0; n1 < R1; ++n1) {
-    const size_t r = col + (size_t)(R2 * n1 + t) * Hx;
-    f[n1] = spec[r];
-    o[n1] = sobs[r];
+    for (int n1 = 0; n1 < R1; ++n1) o[n1] = sobs[col + (size_t)(R2 * n1 + t) * Hx];
+    fft_col<R1, R2>(o, t, sb[g], tw);
+#pragma unroll
+    for (int q = 0; q < R1; ++q) so[q][threadIdx.x] = o[q];
   }
+#pragma unroll
+  for (int n1 = 0; n1 < R1; ++n1) f[n1] = spec[col + (size_t)(R2 * n1 + t) * Hx];
   fft_col<R1, R2>(f, t, sb[g], tw);
-  fft_col<R1, R2>(o, t, sb[g], tw);
   const CtfP P = ctfp[i];
   const float gsc = 2.0f / ((float)D * (float)D), ps = 1.0f / ((float)D * (float)D);
   const bool nx = 2 * kx == D;
@@ -275,11 +279,11 @@ __global__ void __launch_bounds__(kColThreads) k_ctf_colspec(CfgDev c, const Ctf
         C += ctf_raw(P, fx * fx + fy * fy, fx * fx - fy * fy, 2.0 * fx * fy);
       }
     if (nx || ny) C *= (nx && ny) ? 0.25f : 0.5f;
-    const float2 F = f[q], Ob = o[q];
+    const float2 F = f[q], Ob = so[q][threadIdx.x];
     const float Rr = C * F.x - Ob.x, Ri = C * F.y - Ob.y;
     lsum = fmaf(wgt, fmaf(Rr, Rr, Ri * Ri), lsum);
     f[q] = make_float2(gsc * C * Rr, gsc * C * Ri);
-    o[q] = make_float2(C * F.x * ps, C * F.y * ps);
+    so[q][threadIdx.x] = make_float2(C * F.x * ps, C * F.y * ps);
   }
   // inverse column DFT (unnormalised) = conj(DFT(conj(.))), back into row-spectrum order
   auto inverse_store = [&](float2 (&v)[R1], float2 *dst) {
@@ -302,7 +306,11 @@ __global__ void __launch_bounds__(kColThreads) k_ctf_colspec(CfgDev c, const Ctf
     }
   };
   inverse_store(f, spec);
-  if (spred) inverse_store(o, spred);
+  if (spred) {
+#pragma unroll
+    for (int q = 0; q < R1; ++q) f[q] = so[q][threadIdx.x];
+    inverse_store(f, spred);
+  }
   double ls = act ? (double)lsum : 0.0;
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, d);
