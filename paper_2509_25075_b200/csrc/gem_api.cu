@@ -106,8 +106,7 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.spec_obs = take(sizeof(float2) * W * H);
   L.spec_pred = take(sizeof(float2) * W * H);
   L.dldi = take(sizeof(float) * W * D * D);
-  L.slot_a = take(sizeof(float4) * W * N);   // backward image-space partials [i][j]
-  L.slot_b = take(sizeof(float2) * W * N);
+  L.slots = take(sizeof(float) * 10 * (size_t)bwd_chunks((int)W) * N);   // backward world-frame sums [chunk][10][j]
   L.acc = take(sizeof(float4) * 3 * N);
   L.loss_part = take(sizeof(double) * Bm * (size_t)L.loss_blocks);
   L.ctf_par = take(ctf_par_bytes() * Bm);
@@ -456,11 +455,10 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     if (ctx->fused) {
       {
         Prof p(ctx, s, P_RENDER_BWD);
-        launch_render_bwd(c, nb, rec, dldi, at<float4>(ctx, L.slot_a), at<float2>(ctx, L.slot_b), s, ctx->launches);
+        launch_render_bwd(c, nb, rec, dldi, rw, at<float>(ctx, L.slots), s, ctx->launches);
       }
       Prof p(ctx, s, P_BWD_REDUCE);
-      launch_bwd_reduce(c, nb, at<float4>(ctx, L.slot_a), at<float2>(ctx, L.slot_b),
-                        (const float4 *)params->mean_rho, rw, acc, s, ctx->launches);
+      launch_bwd_reduce(c, nb, at<float>(ctx, L.slots), (const float4 *)params->mean_rho, acc, s, ctx->launches);
     }
   }
   ctx->last_p0 = p0 - ctx->W;
@@ -493,12 +491,11 @@ gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_
     CK(cudaMemsetAsync(acc, 0, sizeof(float4) * 3 * (size_t)c.N, s));
     {
       Prof p(ctx, s, P_RENDER_BWD);
-      launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<float>(ctx, L.dldi), at<float4>(ctx, L.slot_a),
-                        at<float2>(ctx, L.slot_b), s, ctx->launches);
+      launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<float>(ctx, L.dldi), at<float>(ctx, L.stage_rot),
+                        at<float>(ctx, L.slots), s, ctx->launches);
     }
     Prof p(ctx, s, P_BWD_REDUCE);
-    launch_bwd_reduce(c, ctx->last_B, at<float4>(ctx, L.slot_a), at<float2>(ctx, L.slot_b),
-                      (const float4 *)params->mean_rho, at<float>(ctx, L.stage_rot), acc, s, ctx->launches);
+    launch_bwd_reduce(c, ctx->last_B, at<float>(ctx, L.slots), (const float4 *)params->mean_rho, acc, s, ctx->launches);
   }
   Prof pf(ctx, s, P_FINALIZE);
   launch_finalize(c, acc, (const float4 *)params->mean_rho, (const float4 *)params->log_scale,

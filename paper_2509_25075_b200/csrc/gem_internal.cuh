@@ -38,7 +38,7 @@ struct __align__(16) SplatRec {
 };
 
 struct Layout {  // byte offsets into the caller's workspace
-  size_t prep, rec, box, hist, subcnt, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slot_a, slot_b, acc, loss_part, ctf_par,
+  size_t prep, rec, box, hist, subcnt, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slots, acc, loss_part, ctf_par,
       stats, ticket, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, cufft_work2, zs_tmp, zs_key, zs_queue, total;
   int64_t n_hist;       // B_max * NT * C
   int64_t n_scan_blk;
@@ -181,10 +181,11 @@ void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double 
                         cudaStream_t s,
                         int &launches);
 int ctf_loss_blocks(int D);
-void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float *dldi, float4 *slotA, float2 *slotB,
+int bwd_chunks(int B);   // particle chunks of the backward (slots per Gaussian)
+void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float *dldi, const float *rot, float *slots,
                        cudaStream_t s, int &launches);
-void launch_bwd_reduce(const CfgDev &c, int B, const float4 *slotA, const float2 *slotB,
-                       const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s, int &launches);
+void launch_bwd_reduce(const CfgDev &c, int B, const float *slots, const float4 *mean_rho, float4 *acc, cudaStream_t s,
+                       int &launches);
 void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho, const float4 *log_scale,
                      const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
                      int &launches);

@@ -426,33 +426,44 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
 }
 
 // Backward ("gradient computation restricted to the Gaussians contributing to each pixel",
-// PAPER.md:108, :117), Gaussian-parallel: one thread per (particle i, Gaussian j) with a
-// non-empty AABB walks the whole box (no tiles, no lists) with the forward's recurrences,
-// two rows at a time (packed fp32), reading g = dL/dI_hat through L1/L2 (ids are in Morton
-// order, so the 32 boxes of a warp are spatial neighbours and their reads share cache lines).
-// Per row pair it accumulates packed sums of h = g e, h k, h k^2 (k = column offset), folds
-// them with dy into six moments, from which the six 2D partials (L_amp, L_mx, L_my, L_a, L_b,
-// L_c) follow algebraically and reduce to the image-space gradient (q0 = L_amp amp, l_mx,
-// l_my, G_hat 00/01/11, in Angstrom units), written to slot (i, j): one writer per slot, a
-// coalesced store, no atomics; k_bwd_reduce sums over i in a fixed order (deterministic).
-constexpr int kBwdBlock = 256;
+// PAPER.md:108, :117), Gaussian-parallel: one thread per (Gaussian j, chunk of kBwdP particles)
+// walks the whole box of (i, j) for each particle i of its chunk in turn (no tiles, no lists)
+// with the forward's recurrences, two rows at a time (packed fp32), reading g = dL/dI_hat
+// through L1/L2 (ids are in Morton order, so the 32 boxes of a warp are spatial neighbours and
+// their reads share cache lines).  Per row pair it accumulates packed sums of h = g e, h k,
+// h k^2 (k = column offset), folds them with dy into six moments, from which the six 2D
+// partials (L_amp, L_mx, L_my, L_a, L_b, L_c) follow algebraically and reduce to the
+// image-space gradient (q0 = L_amp amp, l_mx, l_my, G_hat 00/01/11, in Angstrom units).  That is
+// transformed to the world frame with W_i = P_i^T and summed over the chunk in particle order:
+//   G_mu += W^T (l_mx, l_my, 0),  G_Sigma += W^T [G_hat 0; 0 0] W,  L_rho += q0 / rho,
+// and the chunk's ten sums go to slot (chunk, j) (coalesced, one writer); k_bwd_reduce adds the
+// chunks in a fixed order: deterministic, no atomics, 10 floats per (chunk, j) of traffic
+// instead of 6 per (i, j).
+constexpr int kBwdBlock = 256, kBwdP = 8;   // threads per block, particles per thread
 
 template <bool MK>
-__global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, const SplatRec *__restrict__ rec,
-                                                          const float *__restrict__ dldi, float4 *__restrict__ slotA,
-                                                          float2 *__restrict__ slotB) {
+__global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const SplatRec *__restrict__ rec,
+                                                          const float *__restrict__ dldi,
+                                                          const float *__restrict__ rot, float *__restrict__ slots) {
   constexpr float nh = -0.5f * kLog2e;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+  __shared__ float sW[kBwdP][6];   // rows 0 and 1 of W_i = P_i^T for the chunk's particles
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, chunk = blockIdx.y;
+  const int i0 = chunk * kBwdP, np = min(kBwdP, B - i0);
+  if (threadIdx.x < 6 * np) {
+    const int p = threadIdx.x / 6, e = threadIdx.x % 6;
+    sW[p][e] = rot[9 * (i0 + p) + 3 * (e % 3) + e / 3];   // W[row][col] = P[3 col + row], row = e / 3
+  }
+  __syncthreads();
   if (j >= c.N) return;
+  float vacc[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+  for (int p = 0; p < np; ++p) {
+  const int i = i0 + p;
   const size_t ij = (size_t)i * c.N + j;
   const SplatRec rr = rec[ij];
   const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
   const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
-  if (ulo > uhi || vlo > vhi) {   // culled: zero slot (the reducer reads every slot)
-    slotA[ij] = make_float4(0.f, 0.f, 0.f, 0.f);
-    slotB[ij] = make_float2(0.f, 0.f);
-    return;
-  }
+  if (ulo > uhi || vlo > vhi) continue;   // culled: contributes nothing
   const int wd = uhi - ulo + 1, ht = vhi - vlo + 1;
   const float ka = rr.f0.z, kb = rr.f0.w, kc = rr.f1.x, amp = rr.f1.y;
   const float na = nh * ka, nb2 = 2.f * nh * kb, nc = nh * kc;
@@ -554,64 +565,40 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, const SplatR
   const float G00 = (-(KG00 * ka + KG01 * kb) - hl * ka) * inv_px2;
   const float G01 = (-(KG00 * kb + KG01 * kc) - hl * kb) * inv_px2;
   const float G11 = (-(KG10 * kb + KG11 * kc) - hl * kc) * inv_px2;
-  slotA[ij] = make_float4(La * amp, Lmx * inv_px, Lmy * inv_px, G00);
-  slotB[ij] = make_float2(G01, G11);
+  // world frame, summed over the chunk in particle order
+  const float W0[3] = {sW[p][0], sW[p][1], sW[p][2]}, W1[3] = {sW[p][3], sW[p][4], sW[p][5]};
+  const float lmx = Lmx * inv_px, lmy = Lmy * inv_px;
+  vacc[0] += La * amp;
+  vacc[1] += lmx * W0[0] + lmy * W1[0];
+  vacc[2] += lmx * W0[1] + lmy * W1[1];
+  vacc[3] += lmx * W0[2] + lmy * W1[2];
+  float t0[3], t1[3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l) { t0[l] = G00 * W0[l] + G01 * W1[l]; t1[l] = G01 * W0[l] + G11 * W1[l]; }
+  vacc[4] += W0[0] * t0[0] + W1[0] * t1[0];
+  vacc[5] += W0[0] * t0[1] + W1[0] * t1[1];
+  vacc[6] += W0[0] * t0[2] + W1[0] * t1[2];
+  vacc[7] += W0[1] * t0[1] + W1[1] * t1[1];
+  vacc[8] += W0[1] * t0[2] + W1[1] * t1[2];
+  vacc[9] += W0[2] * t0[2] + W1[2] * t1[2];
+  }
+  float *dst = slots + (size_t)chunk * 10 * c.N + j;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) dst[(size_t)k * c.N] = vacc[k];
 }
 
-// Per-Gaussian reduction of the image-space slots over the particles of a launch, in a fixed
-// order (deterministic), transformed to world frame with W_i = P_i^T and added to acc:
-//   G_mu += W^T (l_mx, l_my, 0),  G_Sigma += W^T [G_hat 0; 0 0] W,  L_rho += q0 / rho.
-constexpr int kRedG = 8, kRedJ = 32;   // particle groups x Gaussians per block
-
-__global__ void __launch_bounds__(kRedG * kRedJ) k_bwd_reduce(int B, int N, const float4 *__restrict__ slotA,
-                                                              const float2 *__restrict__ slotB,
-                                                              const float4 *__restrict__ mean_rho,
-                                                              const float *__restrict__ rot, float4 *__restrict__ acc) {
-  // thread (g, jl): Gaussian j = kRedJ blockIdx.x + jl, particles i = g, g + kRedG, ...; the
-  // kRedG partial sums are combined in a fixed order (deterministic)
-  extern __shared__ float srot[];   // B x 6: rows 0 and 1 of W
-  __shared__ float part[kRedG - 1][10][kRedJ];
-  for (int k = threadIdx.x; k < 6 * B; k += blockDim.x) {
-    const int i = k / 6, e = k % 6;
-    srot[k] = rot[9 * i + 3 * (e % 3) + e / 3];   // W[row][col] = P[3 col + row], row = e / 3
-  }
-  __syncthreads();
-  const int jl = threadIdx.x % kRedJ, g = threadIdx.x / kRedJ;
-  const int j = blockIdx.x * kRedJ + jl;
+// Per-Gaussian reduction of the chunk slots in chunk order (deterministic), added to acc:
+//   acc = (L_rho, G_mu) | G_Sigma (xx xy xz yy) | (yz zz); L_rho = sum q0 / rho.
+__global__ void __launch_bounds__(256) k_bwd_reduce(int nchunk, int N, const float *__restrict__ slots,
+                                                    const float4 *__restrict__ mean_rho, float4 *__restrict__ acc) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
   float v[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  if (j < N) {
-#pragma unroll 4
-    for (int i = g; i < B; i += kRedG) {
-      const size_t ij = (size_t)i * N + j;
-      const float4 sa = __ldg(&slotA[ij]);
-      const float2 sb = __ldg(&slotB[ij]);
-      const float *Wr = srot + 6 * i;
-      const float W0[3] = {Wr[0], Wr[1], Wr[2]}, W1[3] = {Wr[3], Wr[4], Wr[5]};
-      const float lmx = sa.y, lmy = sa.z, G00 = sa.w, G01 = sb.x, G11 = sb.y;
-      v[0] += sa.x;
-      v[1] += lmx * W0[0] + lmy * W1[0];
-      v[2] += lmx * W0[1] + lmy * W1[1];
-      v[3] += lmx * W0[2] + lmy * W1[2];
-      float t0[3], t1[3];
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const float *src = slots + (size_t)ch * 10 * N + j;
 #pragma unroll
-      for (int l = 0; l < 3; ++l) { t0[l] = G00 * W0[l] + G01 * W1[l]; t1[l] = G01 * W0[l] + G11 * W1[l]; }
-      v[4] += W0[0] * t0[0] + W1[0] * t1[0];
-      v[5] += W0[0] * t0[1] + W1[0] * t1[1];
-      v[6] += W0[0] * t0[2] + W1[0] * t1[2];
-      v[7] += W0[1] * t0[1] + W1[1] * t1[1];
-      v[8] += W0[1] * t0[2] + W1[1] * t1[2];
-      v[9] += W0[2] * t0[2] + W1[2] * t1[2];
-    }
+    for (int k = 0; k < 10; ++k) v[k] += __ldg(src + (size_t)k * N);
   }
-  if (g > 0)
-#pragma unroll
-    for (int k = 0; k < 10; ++k) part[g - 1][k][jl] = v[k];
-  __syncthreads();
-  if (g > 0 || j >= N) return;
-#pragma unroll
-  for (int k = 0; k < 10; ++k)
-#pragma unroll
-    for (int gg = 0; gg < kRedG - 1; ++gg) v[k] += part[gg][k][jl];
   const float rho = mean_rho[j].w;
   float4 *dst = acc + 3 * (size_t)j;
   float4 a0 = dst[0], a1 = dst[1], a2 = dst[2];
@@ -662,17 +649,19 @@ void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *b
   ++launches;
 }
 
-void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float *dldi, float4 *slotA, float2 *slotB,
+int bwd_chunks(int B) { return (B + kBwdP - 1) / kBwdP; }
+
+void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float *dldi, const float *rot, float *slots,
                        cudaStream_t s, int &launches) {
-  dim3 grid((c.N + kBwdBlock - 1) / kBwdBlock, B);
-  if (pixel_mask(c)) k_render_bwd<true><<<grid, kBwdBlock, 0, s>>>(c, rec, dldi, slotA, slotB);
-  else k_render_bwd<false><<<grid, kBwdBlock, 0, s>>>(c, rec, dldi, slotA, slotB);
+  dim3 grid((c.N + kBwdBlock - 1) / kBwdBlock, bwd_chunks(B));
+  if (pixel_mask(c)) k_render_bwd<true><<<grid, kBwdBlock, 0, s>>>(c, B, rec, dldi, rot, slots);
+  else k_render_bwd<false><<<grid, kBwdBlock, 0, s>>>(c, B, rec, dldi, rot, slots);
   ++launches;
 }
 
-void launch_bwd_reduce(const CfgDev &c, int B, const float4 *slotA, const float2 *slotB,
-                       const float4 *mean_rho, const float *rot, float4 *acc, cudaStream_t s, int &launches) {
-  k_bwd_reduce<<<(c.N + kRedJ - 1) / kRedJ, kRedG * kRedJ, sizeof(float) * 6 * B, s>>>(B, c.N, slotA, slotB, mean_rho, rot, acc);
+void launch_bwd_reduce(const CfgDev &c, int B, const float *slots, const float4 *mean_rho, float4 *acc, cudaStream_t s,
+                       int &launches) {
+  k_bwd_reduce<<<(c.N + 255) / 256, 256, 0, s>>>(bwd_chunks(B), c.N, slots, mean_rho, acc);
   ++launches;
 }
 
