@@ -487,20 +487,23 @@ gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_
   const CfgDev &c = ctx->dc;
   const Layout &L = ctx->L;
   float4 *acc = at<float4>(ctx, L.acc);
-  if (!ctx->fused) {   // fused mode: the forward already scattered every wave into acc
-    CK(cudaMemsetAsync(acc, 0, sizeof(float4) * 3 * (size_t)c.N, s));
+  if (!ctx->fused) {   // one batch: backward, then chunk sums reduced and finalized in one kernel
     {
       Prof p(ctx, s, P_RENDER_BWD);
       launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<float>(ctx, L.dldi), at<float>(ctx, L.stage_rot),
                         at<float>(ctx, L.slots), s, ctx->launches);
     }
     Prof p(ctx, s, P_BWD_REDUCE);
-    launch_bwd_reduce(c, ctx->last_B, at<float>(ctx, L.slots), (const float4 *)params->mean_rho, acc, s, ctx->launches);
+    launch_reduce_finalize(c, ctx->last_B, at<float>(ctx, L.slots), (const float4 *)params->mean_rho,
+                           (const float4 *)params->log_scale, (const float4 *)params->quat, (float4 *)grad->mean_rho,
+                           (float4 *)grad->log_scale, (float4 *)grad->quat, at<DevStats>(ctx, L.stats), s,
+                           ctx->launches);
+  } else {   // fused mode: the forward already reduced every wave into acc
+    Prof pf(ctx, s, P_FINALIZE);
+    launch_finalize(c, acc, (const float4 *)params->mean_rho, (const float4 *)params->log_scale,
+                    (const float4 *)params->quat, (float4 *)grad->mean_rho, (float4 *)grad->log_scale,
+                    (float4 *)grad->quat, at<DevStats>(ctx, L.stats), s, ctx->launches);
   }
-  Prof pf(ctx, s, P_FINALIZE);
-  launch_finalize(c, acc, (const float4 *)params->mean_rho, (const float4 *)params->log_scale,
-                  (const float4 *)params->quat, (float4 *)grad->mean_rho, (float4 *)grad->log_scale,
-                  (float4 *)grad->quat, at<DevStats>(ctx, L.stats), s, ctx->launches);
   CK(cudaGetLastError());
   return GEM_OK;
 }

@@ -186,6 +186,9 @@ void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float 
                        cudaStream_t s, int &launches);
 void launch_bwd_reduce(const CfgDev &c, int B, const float *slots, const float4 *mean_rho, float4 *acc, cudaStream_t s,
                        int &launches);
+void launch_reduce_finalize(const CfgDev &c, int B, const float *slots, const float4 *mean_rho, const float4 *log_scale,
+                            const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
+                            int &launches);
 void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho, const float4 *log_scale,
                      const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
                      int &launches);

@@ -12,13 +12,10 @@
 namespace gem {
 namespace {
 
-__global__ void __launch_bounds__(256) k_finalize(int N, int no_rot, const float4 *__restrict__ acc,
-                                                  const float4 *__restrict__ mr, const float4 *__restrict__ ls,
-                                                  const float4 *__restrict__ q, float4 *__restrict__ g_mr,
-                                                  float4 *__restrict__ g_ls, float4 *__restrict__ g_q, DevStats *st) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= N) return;
-  const float4 a0 = acc[3 * (size_t)j], a1 = acc[3 * (size_t)j + 1], a2 = acc[3 * (size_t)j + 2];
+__device__ __forceinline__ void finalize_j(int j, int no_rot, float4 a0, float4 a1, float4 a2,
+                                           const float4 *__restrict__ mr, const float4 *__restrict__ ls,
+                                           const float4 *__restrict__ q, float4 *__restrict__ g_mr,
+                                           float4 *__restrict__ g_ls, float4 *__restrict__ g_q, DevStats *st) {
   const float4 qq = q[j], ss = ls[j];
   const float rho = mr[j].w;
   const float n = sqrtf(qq.x * qq.x + qq.y * qq.y + qq.z * qq.z + qq.w * qq.w);
@@ -67,6 +64,36 @@ __global__ void __launch_bounds__(256) k_finalize(int N, int no_rot, const float
   g_q[j] = no_rot ? make_float4(0.f, 0.f, 0.f, 0.f) : gq;   // GEM_FLAG_NO_ROTATION: R fixed to I
   const float chk = a0.x + a0.y + a0.z + a0.w + ds[0] + ds[1] + ds[2] + gq.x + gq.y + gq.z + gq.w;
   if (!isfinite(chk)) st->nonfinite = 1;
+}
+
+__global__ void __launch_bounds__(256) k_finalize(int N, int no_rot, const float4 *__restrict__ acc,
+                                                  const float4 *__restrict__ mr, const float4 *__restrict__ ls,
+                                                  const float4 *__restrict__ q, float4 *__restrict__ g_mr,
+                                                  float4 *__restrict__ g_ls, float4 *__restrict__ g_q, DevStats *st) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  finalize_j(j, no_rot, acc[3 * (size_t)j], acc[3 * (size_t)j + 1], acc[3 * (size_t)j + 2], mr, ls, q, g_mr, g_ls,
+             g_q, st);
+}
+
+// One batch (not fused): the backward's chunk sums [chunk][10][N] (render.cu k_render_bwd) are
+// added in chunk order and finalized in the same thread (no accumulator round trip).
+__global__ void __launch_bounds__(256) k_reduce_finalize(int nchunk, int N, int no_rot, const float *__restrict__ slots,
+                                                         const float4 *__restrict__ mr, const float4 *__restrict__ ls,
+                                                         const float4 *__restrict__ q, float4 *__restrict__ g_mr,
+                                                         float4 *__restrict__ g_ls, float4 *__restrict__ g_q,
+                                                         DevStats *st) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  float v[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const float *src = slots + (size_t)ch * 10 * N + j;
+#pragma unroll
+    for (int k = 0; k < 10; ++k) v[k] += __ldg(src + (size_t)k * N);
+  }
+  const float rho = mr[j].w;
+  finalize_j(j, no_rot, make_float4(rho != 0.f ? v[0] / rho : 0.f, v[1], v[2], v[3]), make_float4(v[4], v[5], v[6], v[7]),
+             make_float4(v[8], v[9], 0.f, 0.f), mr, ls, q, g_mr, g_ls, g_q, st);
 }
 
 __device__ __forceinline__ float adam1(float p, float g, float &m, float &v, float lr, float b1, float b2, float eps,
@@ -120,6 +147,14 @@ __global__ void __launch_bounds__(256) k_adam(int N, AdamArgs A) {
 }
 
 }  // namespace
+
+void launch_reduce_finalize(const CfgDev &c, int B, const float *slots, const float4 *mean_rho, const float4 *log_scale,
+                            const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
+                            int &launches) {
+  k_reduce_finalize<<<(c.N + 255) / 256, 256, 0, s>>>(bwd_chunks(B), c.N, c.flags & GEM_FLAG_NO_ROTATION ? 1 : 0, slots,
+                                                      mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
+  ++launches;
+}
 
 void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho, const float4 *log_scale,
                      const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
