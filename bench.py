@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["gem", "reference"], default="gem")
     ap.add_argument("--config", default="R", choices=sorted(synth.CONFIGS))
-    ap.add_argument("--batch", type=int, default=128, help="particles per GPU per step")
+    ap.add_argument("--batch", type=int, default=256, help="particles per GPU per step")
     ap.add_argument("--tile", type=int, default=8)
     ap.add_argument("--state", default="steady", choices=["steady", "init"])
     ap.add_argument("--ring", type=int, default=1024, help="distinct device-resident particles per GPU")

@@ -331,16 +331,16 @@ def test_R_config_full_size(gem, orc):
 
 
 def test_R_config_bench_batch_sampled(gem, orc):
-    """The bench's exact launch configuration (config R, B = 128 particles per step, 8x8 tiles):
+    """The bench's exact launch configuration (config R, B = 256 particles per step, 8x8 tiles):
     lists, projection and per-particle loss of three sampled particles against the oracle, and a
     property for the summed gradient that holds at any size: the batch gradient equals the sum
-    of the gradients of its four 32-particle quarters."""
-    B = 128
+    of the gradients of its four 64-particle quarters."""
+    B = 256
     case = make_case("R", B=B, seed=13)
     g = run_gpu(gem, case, tile=8)
     assert g["stats"]["status"] == 0, g["stats"]
     st = g["st"]
-    for i in (0, 63, 127):
+    for i in (0, 127, 255):
         sub = dict(case, rot=case["rot"][i:i + 1], shift=case["shift"][i:i + 1], ctf=case["ctf"][i:i + 1],
                    obs=case["obs"][i:i + 1])
         assert_lists_exact(orc, sub, [st.export_lists(i)], 8)
@@ -349,7 +349,7 @@ def test_R_config_bench_batch_sampled(gem, orc):
         assert abs(g["loss"][i] - o["total"]) < LOSS_TOL * o["total"]
     parts = []
     for q in range(4):
-        sl = slice(32 * q, 32 * q + 32)
+        sl = slice(64 * q, 64 * q + 64)
         sub = dict(case, rot=case["rot"][sl], shift=case["shift"][sl], ctf=case["ctf"][sl], obs=case["obs"][sl])
         parts.append(run_gpu(gem, sub, tile=8)["grad"].astype(np.float64))
     tot = sum(parts)
