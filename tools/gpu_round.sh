@@ -14,7 +14,9 @@ timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/round/bench_$TAG.
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/round/bench_ref_$TAG.json 2> gpurun_out/round/bench_ref_$TAG.err
 CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/round/launches_$TAG.csv $CMD > gpurun_out/round/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_render_fwd" -s 9 -c 1 -o gpurun_out/round/full_$TAG $CMD > gpurun_out/round/ncu_full.log 2>&1
+# skip the observation generator's forwards (ring 1024 / batch) and the warm-up step
+FSKIP=$(( 1024 / ${BATCH:-256} + 1 ))
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_render_fwd" -s $FSKIP -c 1 -o gpurun_out/round/full_$TAG $CMD > gpurun_out/round/ncu_full.log 2>&1
 python tools/ncu_summary.py gpurun_out/round/full_$TAG.ncu-rep 40 > gpurun_out/round/ncu_full_summary_$TAG.txt 2>&1
 python tools/ncu_stalls.py gpurun_out/round/full_$TAG.ncu-rep >> gpurun_out/round/ncu_full_summary_$TAG.txt 2>&1
 tail -2 gpurun_out/round/pytest_gpu.log; tail -2 gpurun_out/round/smoke.log; cat gpurun_out/round/bench_$TAG.json; cat gpurun_out/round/bench_ref_$TAG.json; tail -3 gpurun_out/round/bench_$TAG.err
