@@ -578,3 +578,19 @@ def test_negative_densities(gem, orc, tile):
         assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
     for name, cols in CLASSES.items():
         assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+
+
+@pytest.mark.parametrize("D", [64, 48])
+def test_spectral_paths(gem, orc, D):
+    """The row-column spectral path (D = 64: cuFFT 1D rows + k_ctf_colspec<8, 8>) and the 2D
+    fallback (D = 48: 2D cuFFT + k_ctf_loss) against the oracle: images, prediction, loss and
+    gradients."""
+    case = make_case("T", B=3, seed=29, N=800, D=D)
+    g = run_gpu(gem, case)
+    o = oracle_out(orc, case)
+    for i in range(3):
+        assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
+        assert maxnorm_rel(g["pred"][i], o["pred"][i]) < IMG_TOL
+    assert np.all(np.abs(g["loss"][:-1] - o["loss"]) < LOSS_TOL * o["loss"])
+    for name, cols in CLASSES.items():
+        assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
