@@ -73,6 +73,11 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+# BASELINE.json's configs: what each synthetic workload is shaped like
+SHAPES = {"T": "tiny synthetic", "S": "CryoBench-like small protein", "R": "EMPIAR-10028-shaped ribosome",
+          "P": "EMPIAR-10180-shaped spliceosome", "X": "large-scale stress", "A": "desk-scale round trip"}
+
+
 def measured_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (profiles/traffic.json)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
@@ -386,7 +391,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{w.name}: EMPIAR-10028-shaped, N={w.N} Gaussians, D={w.D}, px={w.px} A",
+        "config": {"workload": f"{w.name}: {SHAPES.get(w.name, 'synthetic')}, N={w.N} Gaussians, D={w.D}, px={w.px} A",
                    "model_state": args.state, "batch_per_gpu": B, "global_batch": B * world, "tile": args.tile,
                    "fused_waves": args.fused, "wave": int(st["wave"]), "zsort": args.zsort, "pixel_mask": args.pixel_mask, "tau": args.tau,
                    "exact_tiles": args.exact_tiles,
