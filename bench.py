@@ -351,6 +351,9 @@ def main():
               "data_ring_gb": ring * (19 + w.D * w.D) * 4 / 1e9,
               "d3_buffers": 0, "paper_gem_peak_gb_10028": 1.54}
 
+    # replicated parameters and moments stay bit-identical (checked after timing)
+    replicas = gem.replicas_identical([tr.params.t, tr.m.t, tr.v.t]) if world > 1 else None
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -401,7 +404,7 @@ def main():
                          f"({ring * w.D * w.D * 4 / 1e6:.0f} MB) exceed the 126 MB L2",
                    "useful_pairs_per_step": pairs, "list_entries_per_step": int(st["entries"])},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-        "memory": memory,
+        "memory": memory, "replicas_identical": replicas,
         "kernels": kernels,
         "kernel_times": "CUDA event pair around each launch group, second pass over the same K steps",
     }

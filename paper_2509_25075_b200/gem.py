@@ -280,6 +280,23 @@ def allreduce_grad(grad: SoA, group=None):
     return grad
 
 
+def replicas_identical(tensors, group=None) -> bool:
+    """the replicated parameters / Adam moments must stay bit-identical across the
+    data-parallel ranks.  A 64-bit checksum of the raw bytes of `tensors` (a diagnostic outside
+    the training step) is all-gathered and compared; True without a process group."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return True
+    h = torch.zeros(1, dtype=torch.int64, device=tensors[0].device)
+    for t in tensors:
+        w = t.detach().contiguous().view(torch.int32).reshape(-1).to(torch.int64)
+        idx = torch.arange(1, w.numel() + 1, device=w.device, dtype=torch.int64)
+        h += (w * idx).sum()                 # position-weighted: permutations change the sum
+    hs = [torch.zeros_like(h) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(hs, h, group=group)
+    return all(bool((x == hs[0]).all()) for x in hs)
+
+
 def shard_indices(n_particles: int, world: int, rank: int, batch: int, step: int, seed: int = 0):
     """Particle ids rank `rank` processes at `step`: a contiguous disjoint shard
     per rank, drawn with a per-epoch seeded permutation."""

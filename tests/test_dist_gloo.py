@@ -47,12 +47,15 @@ def _worker(rank, world, port, outdir):
     p = np.stack(params).astype(np.float64)
     p1, _, _ = oracle.adam(p, g.t.numpy().astype(np.float64), np.zeros_like(p), np.zeros_like(p), 1,
                            [1e-3, 5e-3, 1e-3, 5e-2])
-    h = torch.tensor([float(np.frombuffer(p1.tobytes(), np.uint8).astype(np.int64).sum())], dtype=torch.float64)
-    hs = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
-    dist.all_gather(hs, h)
+    same = gem.replicas_identical([torch.from_numpy(p1.astype(np.float32)), g.t])
+    # a perturbed replica must be detected
+    p2 = p1.astype(np.float32).copy()
+    if rank == 1:
+        p2.flat[7] = np.nextafter(p2.flat[7], np.float32(np.inf))
+    diff = gem.replicas_identical([torch.from_numpy(p2)])
     np.save(os.path.join(outdir, f"g{rank}.npy"), g.t.numpy())
     np.save(os.path.join(outdir, f"idx{rank}.npy"), idx)
-    np.save(os.path.join(outdir, f"h{rank}.npy"), np.array([x.item() for x in hs]))
+    np.save(os.path.join(outdir, f"h{rank}.npy"), np.array([same, diff]))
     dist.destroy_process_group()
 
 
@@ -80,4 +83,4 @@ def test_gloo_allreduce_equals_full_batch(tmp_path, orc):
     assert np.array_equal(g0, g1)                    # every rank holds identical reduced bytes
     assert np.abs(g0 - ref).max() <= 1e-6 * np.abs(ref).max()
     h0 = np.load(tmp_path / "h0.npy")
-    assert h0[0] == h0[1]                             # replicated Adam stays bit-identical
+    assert h0[0] and not h0[1]                        # replicated Adam stays bit-identical; a 1-ulp drift is caught
