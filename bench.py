@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--ring", type=int, default=1024, help="distinct device-resident particles per GPU")
     ap.add_argument("--fused", action="store_true", help="L2-resident wave pipeline (GEM_FLAG_FUSED)")
     ap.add_argument("--wave", type=int, default=0, help="particles per wave (0 = auto)")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="strong scaling: this many particles per step in total, split over the GPUs")
     ap.add_argument("--zsort", action="store_true", help="P:227 z-sorted tile lists (GEM_FLAG_ZSORT)")
     ap.add_argument("--pixel-mask", default="aabb", choices=["aabb", "ellipse", "tau", "ellipse+tau"],
                     help="Eq. 8 per-pixel selection variant (GEM_FLAG_ELLIPSE / GEM_FLAG_PIXEL_TAU)")
@@ -236,7 +238,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     w = synth.CONFIGS[args.config]
-    B = args.batch
+    # weak scaling (default): B particles per GPU; strong scaling: a fixed global batch split
+    B = args.batch if not args.global_batch else max(1, args.global_batch // world)
     ring = max(args.ring // B, 1) * B
     px = float(np.float32(w.px))
     model = synth.steady_model if args.state == "steady" else synth.init_model
@@ -392,7 +395,8 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if args.global_batch else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{w.name}: {SHAPES.get(w.name, 'synthetic')}, N={w.N} Gaussians, D={w.D}, px={w.px} A",
                    "model_state": args.state, "batch_per_gpu": B, "global_batch": B * world, "tile": args.tile,
