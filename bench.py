@@ -386,6 +386,18 @@ def main():
         roof = {"bound": "hbm", "kernel": dominant, "achieved": None, "peak": float(peaks.get("hbm_gbs", 6650.0)),
                 "unit": "GB/s", "frac": None, "traffic": None}
 
+    # SURVEY §8(d) step-level roofline: T_roof = FP32 lane-ops of the method (31 per useful pair:
+    # forward 9 + backward 22, an FMA counted once) at the FP32 peak + the cuFFT/CTF chain's
+    # implementation-minimum HBM bytes (5 D^2 4 + 6 D (D/2+1) 8 per particle) at the HBM peak
+    lane_ops = 31.0 * pairs
+    chain_bytes = B * (5.0 * w.D * w.D * 4 + 6.0 * w.D * (w.D // 2 + 1) * 8)
+    t_fp32 = lane_ops / (148 * 128 * sm_max * 1e6)
+    t_hbm = chain_bytes / (float(peaks.get("hbm_gbs", 6537.6)) * 1e9)
+    t_roof = t_fp32 + t_hbm
+    step_roof = {"t_roof_ms": t_roof * 1e3, "t_step_ms": ms / args.steps, "frac": t_roof / (ms / args.steps / 1e3),
+                 "model": "31 FP32 lane-ops per useful pair at 148 SM x 128 lanes x f_max + cuFFT/CTF chain "
+                          "bytes at the measured HBM copy bandwidth (SURVEY 8(d))"}
+
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -407,7 +419,8 @@ def main():
                          f"{B * w.N * 32 / 1e6:.0f} MB + images) and a {ring}-particle ring "
                          f"({ring * w.D * w.D * 4 / 1e6:.0f} MB) exceed the 126 MB L2",
                    "useful_pairs_per_step": pairs, "list_entries_per_step": int(st["entries"])},
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks,
         "memory": memory, "replicas_identical": replicas,
         "kernels": kernels,
         "kernel_times": "CUDA event pair around each launch group, second pass over the same K steps",
