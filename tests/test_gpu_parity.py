@@ -613,3 +613,43 @@ def test_P_config_sampled(gem, orc):
         got = g["proj"][i][pix[:, 1], pix[:, 0]]
         assert np.abs(got - ref).max() < IMG_TOL * np.abs(g["proj"][i]).max(), i
     assert np.all(np.isfinite(g["loss"])) and np.all(np.isfinite(g["grad"]))
+
+
+def test_flag_combination_zsort_ellipse_no_rotation(gem, orc):
+    """Flags compose: z-sorted AABB lists (f1), the exact-ellipse pixel mask (f1) and the
+    No Rotation ablation (f3) together, against the oracle's O4z lists, masked images, loss and
+    gradients (q = identity, its gradient exactly zero)."""
+    for seed in range(60, 80):
+        case = make_case("T", B=3, seed=seed)
+        mr, ls, q = (a.copy() for a in case["params"])
+        q[:] = [1.0, 0.0, 0.0, 0.0]
+        case = dict(case, params=(mr, ls, q))
+        if mask_ties(orc, case, 2, 0.0) == 0:
+            break
+    else:
+        pytest.fail("no tie-free case")
+    w = case["w"]
+    dev = torch.device("cuda", 0)
+    cfg = gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=3, zsort=True, pixel_mask="ellipse",
+                        ablation="no_rotation")
+    st = gem.GemStep(cfg, dev)
+    P = gem.SoA.from_arrays(*case["params"], device=dev)
+    t = lambda a: torch.from_numpy(a).to(dev)
+    proj = torch.empty(3, w.D, w.D, device=dev)
+    loss = st.forward(P, t(case["rot"]), t(case["shift"]), t(case["ctf"]), t(case["obs"]), proj=proj)
+    grad = gem.SoA.zeros(w.N, dev)
+    st.backward(P, grad)
+    torch.cuda.synchronize()
+    assert assert_zsorted_lists_exact(orc, case, [st.export_lists(i) for i in range(3)], 8) > 0
+    o = orc.loss_grad(case["params"], case["rot"], case["shift"], case["ctf"], case["obs"], w.D, case["px"],
+                      want=("proj",), pixmask=2)
+    pr = proj.cpu().numpy()
+    for i in range(3):
+        assert maxnorm_rel(pr[i], o["proj"][i]) < IMG_TOL, i
+    lo = loss.cpu().numpy()
+    assert np.all(np.abs(lo[:-1] - o["loss"]) < LOSS_TOL * o["loss"])
+    g = grad.t.permute(1, 0, 2).reshape(w.N, 12).cpu().numpy()
+    assert np.all(g[:, 8:12] == 0.0)
+    for name, cols in CLASSES.items():
+        if name != "q":
+            assert maxnorm_rel(g[:, cols], o["grad"][:, cols]) < GRAD_TOL, name
