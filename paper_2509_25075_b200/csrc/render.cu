@@ -430,8 +430,9 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
 // walks the whole box of (i, j) for each particle i of its chunk in turn (no tiles, no lists)
 // with the forward's recurrences, two rows at a time (packed fp32), reading g = dL/dI_hat
 // through L1/L2 (ids are in Morton order, so the 32 boxes of a warp are spatial neighbours and
-// their reads share cache lines).  Per row pair it accumulates packed sums of h = g e, h k,
-// h k^2 (k = column offset), folds them with dy into six moments, from which the six 2D
+// their reads share cache lines).  Per row pair it accumulates packed running sums of h = g e
+// (C, Q, Z below: the zeroth to second column moments without forming h k, h k^2), folds them
+// with dy into six moments, from which the six 2D
 // partials (L_amp, L_mx, L_my, L_a, L_b, L_c) follow algebraically and reduce to the
 // image-space gradient (q0 = L_amp amp, l_mx, l_my, G_hat 00/01/11, in Angstrom units).  That is
 // transformed to the world frame with W_i = P_i^T and summed over the chunk in particle order:
@@ -476,7 +477,12 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const
   // MK: keep a pixel iff e >= ethr (= thr / |amp|, see keep_thr)
   const float ethr = MK ? keep_thr(c, amp, ex2(nh * c.k * c.k)) / fabsf(amp) : 0.f;
   const float *gi = dldi + ((size_t)i * c.D + vlo) * c.D + ulo;
-  float M0 = 0.f, M1 = 0.f, M2 = 0.f, Y0 = 0.f, Y1 = 0.f, YY = 0.f;
+  // Per row the pixel weights h_k (k = 0 .. wd-1) are summed by three running sums,
+  // C += h, Q += C, Z += Q (one packed add each instead of forming h k and h k^2): at the end of
+  // the row C = sum h, Q = sum h t, Z = sum h t (t + 1) / 2 with t = wd - k, from which
+  // sum h k = wd C - Q and sum h k^2 = wd^2 C - 2 wd Q + 2 Z - Q (linear, so the rows are
+  // folded in (C, Q, Z) form and converted once per (i, j)).
+  float M0 = 0.f, MQ = 0.f, MZ = 0.f, Y0 = 0.f, YQ = 0.f, YY = 0.f;
   float El = 0.f, V = 0.f, Rl = 0.f, W = 0.f, Kb = 0.f, S = 0.f;
   if (!slow) {
     El = ex2(f0);
@@ -486,13 +492,14 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const
     Kb = ex2(nb2);
     S = ex2(2.f * na);
   }
-  const float2 S2 = make_float2(S, S), one = make_float2(1.f, 1.f);
+  const float wf = (float)wd;
+  const float2 S2 = make_float2(S, S);
 #pragma unroll 1
   for (int r2 = 0; r2 < ht; r2 += 2) {
     const bool vB = r2 + 1 < ht;
     const float dyA = dy0 + (float)r2, dyB = dyA + 1.f;
     const float *ga = gi + (size_t)r2 * c.D, *gb = ga + c.D;
-    float2 T0 = make_float2(0.f, 0.f), T1 = T0, T2 = T0;
+    float2 C = make_float2(0.f, 0.f), Q = C, Z = C;
     if (!slow) {
       float2 E2, R2;
       E2.x = El;
@@ -501,20 +508,17 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const
       E2.y = vB ? El : 0.f;
       R2.y = vB ? Rl : 0.f;
       if (vB) { El *= V; V *= W; Rl *= Kb; }
-      float2 kk = make_float2(0.f, 0.f);
       // column pairs at even absolute columns are read with one 64-bit load per row (half the
       // L1 requests); an odd first column and an odd last column are peeled
       int k = 0;
       auto step = [&](float gA, float gBv) {
         const float2 Em = MK ? make_float2(E2.x >= ethr ? E2.x : 0.f, E2.y >= ethr ? E2.y : 0.f) : E2;
         const float2 h = __fmul2_rn(make_float2(gA, gBv), Em);
-        const float2 hk = __fmul2_rn(h, kk);
-        T0 = __fadd2_rn(T0, h);
-        T1 = __fadd2_rn(T1, hk);
-        T2 = __ffma2_rn(hk, kk, T2);
+        C = __fadd2_rn(C, h);
+        Q = __fadd2_rn(Q, C);
+        Z = __fadd2_rn(Z, Q);
         E2 = __fmul2_rn(E2, R2);
         R2 = __fmul2_rn(R2, S2);
-        kk = __fadd2_rn(kk, one);
       };
       if (ulo & 1) {
         step(__ldg(ga), vB ? __ldg(gb) : 0.f);
@@ -528,31 +532,33 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const
         step(a2.y, b2.y);
       }
       if (k < wd) step(__ldg(ga + k), vB ? __ldg(gb + k) : 0.f);
-    } else {   // direct evaluation, exp per pixel
+    } else {   // direct evaluation, exp per pixel; sums converted to (C, Q, Z) form
       const float fA = fmaf(dyA, fmaf(nc, dyA, Gx), Fx), fB = fmaf(dyB, fmaf(nc, dyB, Gx), Fx);
       const float gA = fmaf(nb2, dyA, D0), gB = fmaf(nb2, dyB, D0);
 #pragma unroll 1
       for (int k = 0; k < wd; ++k) {
-        const float kf = (float)k, kq = kf * (kf - 1.f) * na;
+        const float tf = wf - (float)k, kf = (float)k, kq = kf * (kf - 1.f) * na;
         float eA = ex2(fmaf(kf, gA, fA) + kq), eB = ex2(fmaf(kf, gB, fB) + kq);
         if (MK) { eA = eA >= ethr ? eA : 0.f; eB = eB >= ethr ? eB : 0.f; }
         const float hA = __ldg(ga + k) * eA;
         const float hB = vB ? __ldg(gb + k) * eB : 0.f;
-        T0.x += hA; T0.y += hB;
-        T1.x = fmaf(hA, kf, T1.x); T1.y = fmaf(hB, kf, T1.y);
-        T2.x = fmaf(hA * kf, kf, T2.x); T2.y = fmaf(hB * kf, kf, T2.y);
+        const float zt = 0.5f * tf * (tf + 1.f);
+        C.x += hA; C.y += hB;
+        Q.x = fmaf(hA, tf, Q.x); Q.y = fmaf(hB, tf, Q.y);
+        Z.x = fmaf(hA, zt, Z.x); Z.y = fmaf(hB, zt, Z.y);
       }
     }
-    M0 += T0.x + T0.y;
-    M1 += T1.x + T1.y;
-    M2 += T2.x + T2.y;
-    Y0 = fmaf(dyA, T0.x, fmaf(dyB, T0.y, Y0));
-    Y1 = fmaf(dyA, T1.x, fmaf(dyB, T1.y, Y1));
-    YY = fmaf(dyA * dyA, T0.x, fmaf(dyB * dyB, T0.y, YY));
+    M0 += C.x + C.y;
+    MQ += Q.x + Q.y;
+    MZ += Z.x + Z.y;
+    Y0 = fmaf(dyA, C.x, fmaf(dyB, C.y, Y0));
+    YQ = fmaf(dyA, Q.x, fmaf(dyB, Q.y, YQ));
+    YY = fmaf(dyA * dyA, C.x, fmaf(dyB * dyB, C.y, YY));
   }
-  // k-moments -> dx-moments (dx = dx0 + k)
-  const float A0 = M0, A1 = fmaf(dx0, M0, M1), A2 = fmaf(dx0, fmaf(dx0, M0, 2.f * M1), M2);
-  const float Ay0 = Y0, Ay1 = fmaf(dx0, Y0, Y1), Ayy0 = YY;
+  // (C, Q, Z) moments -> dx-moments: dx = dx0 + k = dxw - t with dxw = dx0 + wd
+  const float dxw = dx0 + wf, Mt2 = fmaf(2.f, MZ, -MQ);   // Mt2 = sum h t^2
+  const float A0 = M0, A1 = fmaf(dxw, M0, -MQ), A2 = fmaf(dxw, fmaf(dxw, M0, -2.f * MQ), Mt2);
+  const float Ay0 = Y0, Ay1 = fmaf(dxw, Y0, -YQ), Ayy0 = YY;
   const float La = A0;
   const float Lmx = amp * fmaf(ka, A1, kb * Ay0), Lmy = amp * fmaf(kb, A1, kc * Ay0);
   const float Lpa = -0.5f * amp * A2, Lpb = -amp * Ay1, Lpc = -0.5f * amp * Ayy0;
