@@ -513,8 +513,7 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const
       int k = 0;
       auto step = [&](float gA, float gBv) {
         const float2 Em = MK ? make_float2(E2.x >= ethr ? E2.x : 0.f, E2.y >= ethr ? E2.y : 0.f) : E2;
-        const float2 h = __fmul2_rn(make_float2(gA, gBv), Em);
-        C = __fadd2_rn(C, h);
+        C = __ffma2_rn(make_float2(gA, gBv), Em, C);   // C += h, h = g e
         Q = __fadd2_rn(Q, C);
         Z = __fadd2_rn(Z, Q);
         E2 = __fmul2_rn(E2, R2);
