@@ -230,8 +230,9 @@ constexpr int kColThreads = 128;
 
 template <int R1, int R2>
 __global__ void __launch_bounds__(kColThreads) k_ctf_colspec(CfgDev c, const CtfP *__restrict__ ctfp,
-                                                             float2 *__restrict__ spec, const float2 *__restrict__ sobs,
-                                                             float2 *__restrict__ spred, double *__restrict__ part) {
+                                                             const float2 *__restrict__ spec,
+                                                             const float2 *__restrict__ sobs, float2 *__restrict__ spred,
+                                                             float2 *__restrict__ zout, double *__restrict__ part) {
   constexpr int D = R1 * R2, S = R1 / R2, G = kColThreads / R2, Hx = D / 2 + 1;
   __shared__ float2 tw[D];
   __shared__ float2 sb[G][R1 * (R2 + 1)];
@@ -305,7 +306,44 @@ __global__ void __launch_bounds__(kColThreads) k_ctf_colspec(CfgDev c, const Ctf
       }
     }
   };
-  inverse_store(f, spec);
+  // gradient: rows (2m, 2m + 1) of the row spectrum, A and B, packed as one complex row
+  // Z_m = A + i B over all D columns (A[D - kx] = conj A[kx]); the inverse C2C of Z_m is then
+  // (g[2m][u], g[2m + 1][u]) interleaved: the layout k_render_bwd reads.  The imaginary parts
+  // at kx = 0 and D/2 are dropped (what a C2R of the Hermitian half spectrum computes).
+  {
+#pragma unroll
+    for (int q = 0; q < R1; ++q) {
+      const int ky = (t * S + q / R2) + R1 * (q % R2);
+      sb[g][ky] = make_float2(f[q].x, -f[q].y);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) f[n1] = sb[g][R2 * n1 + t];
+    __syncwarp();
+    fft_col<R1, R2>(f, t, sb[g], tw);   // conj(f[q]) = row-spectrum value of row(q), column kx
+    float2 *zi = zout + (size_t)i * (D / 2) * D;
+    auto put = [&](int m, float2 A, float2 B) {   // A = row 2m, B = row 2m + 1 (column kx)
+      if (kx == 0 || nx) {
+        zi[(size_t)m * D + kx] = make_float2(A.x, B.x);
+      } else {
+        zi[(size_t)m * D + kx] = make_float2(A.x - B.y, A.y + B.x);
+        zi[(size_t)m * D + (D - kx)] = make_float2(A.x + B.y, B.x - A.y);
+      }
+    };
+    if constexpr (S == 2) {   // row(q) = 2t + R1 q for q < R2, its partner row(q + R2) = row(q) + 1
+#pragma unroll
+      for (int q = 0; q < R2; ++q)
+        if (act)
+          put(t + (R1 / 2) * q, make_float2(f[q].x, -f[q].y), make_float2(f[q + R2].x, -f[q + R2].y));
+    } else {   // S == 1: row(q) = t + R1 q, the partner row is in lane t ^ 1 of the group
+#pragma unroll
+      for (int q = 0; q < R1; ++q) {
+        const float2 mine = make_float2(f[q].x, -f[q].y);
+        const float2 other = make_float2(__shfl_xor_sync(0xffffffffu, mine.x, 1), __shfl_xor_sync(0xffffffffu, mine.y, 1));
+        if (act && !(t & 1)) put((t >> 1) + (R1 / 2) * q, mine, other);
+      }
+    }
+  }
   if (spred) {
 #pragma unroll
     for (int q = 0; q < R1; ++q) f[q] = so[q][threadIdx.x];
@@ -337,14 +375,15 @@ void launch_ctf_params(const CfgDev &c, int B, const float *ctf, void *ctf_par, 
 bool spectral_rows(int D) { return D == 32 || D == 64 || D == 128 || D == 256; }
 
 void launch_ctf_loss(const CfgDev &c, int B, const void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
-                     float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches) {
+                     float2 *spec_pred, float2 *zout, double *loss_part, int loss_blocks, cudaStream_t s,
+                     int &launches) {
   const CtfP *P = reinterpret_cast<const CtfP *>(ctf_par);
   dim3 grid(loss_blocks, B);
   switch (spectral_rows(c.D) ? c.D : 0) {
-    case 32: k_ctf_colspec<8, 4><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part); break;
-    case 64: k_ctf_colspec<8, 8><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part); break;
-    case 128: k_ctf_colspec<16, 8><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part); break;
-    case 256: k_ctf_colspec<16, 16><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part); break;
+    case 32: k_ctf_colspec<8, 4><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, zout, loss_part); break;
+    case 64: k_ctf_colspec<8, 8><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, zout, loss_part); break;
+    case 128: k_ctf_colspec<16, 8><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, zout, loss_part); break;
+    case 256: k_ctf_colspec<16, 16><<<grid, kColThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, zout, loss_part); break;
     default: k_ctf_loss<<<grid, kCtfThreads, 0, s>>>(c, P, spec_hat, spec_obs, spec_pred, loss_part);
   }
   ++launches;

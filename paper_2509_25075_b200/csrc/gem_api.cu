@@ -62,11 +62,17 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
 
 // 2D plans, or -- on the row-column spectral path (spectral_rows(D), see ctf_loss.cu) -- 1D
 // plans over the B*D rows of the batch (R2C: real rows of D -> D/2+1 bins; C2R the reverse)
-bool make_plan(int D, int B, cufftType type, cufftHandle *h, size_t *ws) {
+// il: the inverse of dL/dI for the backward on the row path: a C2C of length D over the B D / 2
+// packed row pairs Z_m = A + i B written by k_ctf_colspec; its output (g[2m][u], g[2m + 1][u])
+// is the row-pair interleaved layout k_render_bwd reads
+bool make_plan(int D, int B, cufftType type, cufftHandle *h, size_t *ws, bool il = false) {
   if (cufftCreate(h) != CUFFT_SUCCESS) return false;
   if (cufftSetAutoAllocation(*h, 0) != CUFFT_SUCCESS) { cufftDestroy(*h); return false; }
   cufftResult r;
-  if (spectral_rows(D)) {
+  if (il) {
+    int n[1] = {D};
+    r = cufftMakePlanMany(*h, 1, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_C2C, B * D / 2, ws);
+  } else if (spectral_rows(D)) {
     int n[1] = {D};
     const int Hx = D / 2 + 1;
     const bool fwd = type == CUFFT_R2C;
@@ -133,6 +139,12 @@ bool cufft_sizes(int D, int B, size_t *bytes) {
   if (!make_plan(D, B, CUFFT_C2R, &b, &wb)) { cufftDestroy(a); return false; }
   cufftDestroy(a);
   cufftDestroy(b);
+  if (spectral_rows(D)) {
+    size_t wi = 0;
+    if (!make_plan(D, B, CUFFT_C2R, &b, &wi, true)) return false;
+    cufftDestroy(b);
+    if (wi > wb) wb = wi;
+  }
   *bytes = (wa > wb ? wa : wb) + 4096;
   return true;
 }
@@ -149,12 +161,14 @@ bool soa_aligned(const gem_soa *s) {
   return aligned16(s->mean_rho) && aligned16(s->log_scale) && aligned16(s->quat);
 }
 
-gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r, cufftHandle *r2c_obs) {
+gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r, cufftHandle *r2c_obs,
+                    cufftHandle *c2r_il) {
   for (int k = 0; k < ctx->n_plans; ++k)
     if (ctx->plan_B[k] == B) {
       *r2c = ctx->plan_r2c[k];
       *c2r = ctx->plan_c2r[k];
       *r2c_obs = ctx->plan_obs[k];
+      *c2r_il = ctx->plan_il[k];
       return GEM_OK;
     }
   int slot = ctx->n_plans < 8 ? ctx->n_plans : 7;
@@ -162,6 +176,7 @@ gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r, cuf
     cufftDestroy(ctx->plan_r2c[7]);
     cufftDestroy(ctx->plan_c2r[7]);
     cufftDestroy(ctx->plan_obs[7]);
+    if (ctx->plan_il[7]) cufftDestroy(ctx->plan_il[7]);
     ctx->n_plans = 7;
   }
   size_t wa = 0, wb = 0, wc = 0;
@@ -176,6 +191,16 @@ gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r, cuf
     cufftDestroy(a); cufftDestroy(b); cufftDestroy(o);
     return GEM_E_CUFFT;
   }
+  cufftHandle il = 0;
+  if (spectral_rows(ctx->dc.D)) {
+    size_t wi = 0;
+    if (!make_plan(ctx->dc.D, B, CUFFT_C2R, &il, &wi, true) || wi > cap || cufftSetWorkArea(il, work) != CUFFT_SUCCESS) {
+      if (il) cufftDestroy(il);
+      cufftDestroy(a); cufftDestroy(b); cufftDestroy(o);
+      return GEM_E_CUFFT;
+    }
+  }
+  ctx->plan_il[slot] = il;
   ctx->plan_B[slot] = B;
   ctx->plan_r2c[slot] = a;
   ctx->plan_c2r[slot] = b;
@@ -184,6 +209,7 @@ gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r, cuf
   *r2c = a;
   *c2r = b;
   *r2c_obs = o;
+  *c2r_il = il;
   return GEM_OK;
 }
 
@@ -283,8 +309,8 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
     delete ctx;
     return GEM_E_CUDA;
   }
-  cufftHandle a, b, o;
-  gem_status st = plan_for(ctx, c.wave, &a, &b, &o);
+  cufftHandle a, b, o, il;
+  gem_status st = plan_for(ctx, c.wave, &a, &b, &o, &il);
   if (st != GEM_OK) { gem_destroy(ctx); return st; }
   if (cudaMemsetAsync(ctx->ws + L.stats, 0, sizeof(DevStats), ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(ctx->ws + L.ticket, 0, 64, ctx->stream) != cudaSuccess ||
@@ -305,6 +331,7 @@ gem_status gem_destroy(gem_ctx *ctx) {
     cufftDestroy(ctx->plan_r2c[k]);
     cufftDestroy(ctx->plan_c2r[k]);
     cufftDestroy(ctx->plan_obs[k]);
+    if (ctx->plan_il[k]) cufftDestroy(ctx->plan_il[k]);
   }
   if (ctx->side) {
     cudaStreamSynchronize(ctx->side);
@@ -400,8 +427,8 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
   int p0 = 0, nb = 0;
   for (p0 = 0; p0 < B; p0 += ctx->W) {   // one wave (all of B when not fused)
     nb = B - p0 < ctx->W ? B - p0 : ctx->W;
-    cufftHandle r2c, c2r, r2c_obs;
-    gem_status ps = plan_for(ctx, nb, &r2c, &c2r, &r2c_obs);
+    cufftHandle r2c, c2r, r2c_obs, c2r_il;
+    gem_status ps = plan_for(ctx, nb, &r2c, &c2r, &r2c_obs, &c2r_il);
     if (ps != GEM_OK) return ps;
     // fork: the observed images' R2C and the per-particle CTF constants run on the internal side
     // stream, overlapped with the splat / binning / render of this wave; joined before the
@@ -443,14 +470,26 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     {
       Prof p(ctx, s, P_CTF_LOSS);
-      launch_ctf_loss(c, nb, ctx->ws + L.ctf_par, sh, so, pred_out ? sp : nullptr, lpart + (size_t)p0 * L.loss_blocks,
+      launch_ctf_loss(c, nb, ctx->ws + L.ctf_par, sh, so, pred_out ? sp : nullptr,
+                      c2r_il ? at<float2>(ctx, L.proj) : nullptr, lpart + (size_t)p0 * L.loss_blocks,
                       L.loss_blocks, s, ctx->launches);
     }
     CK(cudaEventRecord(ctx->ev_ctf, s));
     {
       Prof p(ctx, s, P_FFT_C2R);
       if (pred_out) CKF(cufftExecC2R(c2r, (cufftComplex *)sp, (cufftReal *)(pred_out + p0 * DD)));
-      CKF(cufftExecC2R(c2r, (cufftComplex *)sh, (cufftReal *)dldi));
+      // dL/dI in the backward's row-pair interleaved layout: on the row path the column kernel
+      // wrote the packed row pairs Z into the proj region (dead after the R2C; unused when the
+      // caller takes the projections) and one C2C inverts them; otherwise the 2D C2R writes
+      // row-major into the proj region and k_dldi_pack interleaves
+      if (c2r_il) {
+        CKF(cufftSetStream(c2r_il, s));
+        CKF(cufftExecC2C(c2r_il, at<cufftComplex>(ctx, L.proj), (cufftComplex *)dldi, CUFFT_INVERSE));
+      } else {
+        float *raw = at<float>(ctx, L.proj);
+        CKF(cufftExecC2R(c2r, (cufftComplex *)sh, (cufftReal *)raw));
+        launch_dldi_pack(c, nb, raw, dldi, s, ctx->launches);
+      }
     }
     if (ctx->fused) {
       {

@@ -87,6 +87,7 @@ struct gem_ctx {
   // cuFFT plans keyed by batch size (small cache)
   int plan_B[8];
   cufftHandle plan_r2c[8], plan_c2r[8], plan_obs[8];   // plan_obs: R2C of the observed images (side stream)
+  cufftHandle plan_il[8];   // C2C of the packed dL/dI row pairs (row path only, else 0)
   cudaStream_t side;   // internal stream: observed-image R2C overlapped with splat/bin/render
   cudaEvent_t ev_fork, ev_join, ev_ctf, ev_loss;   // side-stream fork / join points
   int n_plans;
@@ -174,13 +175,15 @@ void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *b
                        int *ticket, cudaStream_t s, int &launches);
 void launch_ctf_params(const CfgDev &c, int B, const float *ctf, void *ctf_par, cudaStream_t s, int &launches);
 void launch_ctf_loss(const CfgDev &c, int B, const void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
-                     float2 *spec_pred, double *loss_part, int loss_blocks, cudaStream_t s, int &launches);
+                     float2 *spec_pred, float2 *zout, double *loss_part, int loss_blocks, cudaStream_t s,
+                     int &launches);
 size_t ctf_par_bytes();
 bool spectral_rows(int D);   // row-column spectral path (1D row plans + column kernel)
 void launch_loss_reduce(int B, const double *loss_part, int loss_blocks, double *loss, DevStats *st, int *ticket,
                         cudaStream_t s,
                         int &launches);
 int ctf_loss_blocks(int D);
+void launch_dldi_pack(const CfgDev &c, int B, const float *in, float *out, cudaStream_t s, int &launches);
 int bwd_chunks(int B);   // particle chunks of the backward (slots per Gaussian)
 void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float *dldi, const float *rot, float *slots,
                        cudaStream_t s, int &launches);

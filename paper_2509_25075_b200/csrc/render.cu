@@ -476,9 +476,10 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const
   const bool slow = !(fminf(f0, f1) >= -100.f && fminf(r0, r1) >= -120.f && nc >= -60.f && fabsf(nb2) <= 120.f);
   // MK: keep a pixel iff e >= ethr (= thr / |amp|, see keep_thr)
   const float ethr = MK ? keep_thr(c, amp, ex2(nh * c.k * c.k)) / fabsf(amp) : 0.f;
-  const float *gi = dldi + ((size_t)i * c.D + vlo) * c.D + ulo;
+  // dL/dI in row-pair interleaved layout (k_dldi_pack): pair m, column u holds (g[2m][u], g[2m+1][u])
+  const float *gi = dldi + (size_t)i * c.D * c.D + ((size_t)(vlo >> 1) * c.D + ulo) * 2;
   // Per row the pixel weights h_k (k = 0 .. wd-1) are summed by three running sums,
-  // C += h, Q += C, Z += Q (one packed add each instead of forming h k and h k^2): at the end of
+  // C += h, Q += C, Z += Q (one packed op each instead of forming h k and h k^2): at the end of
   // the row C = sum h, Q = sum h t, Z = sum h t (t + 1) / 2 with t = wd - k, from which
   // sum h k = wd C - Q and sum h k^2 = wd^2 C - 2 wd Q + 2 Z - Q (linear, so the rows are
   // folded in (C, Q, Z) form and converted once per (i, j)).
@@ -494,43 +495,44 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const
   }
   const float wf = (float)wd;
   const float2 S2 = make_float2(S, S);
+  // row pairs at absolute (2m, 2m + 1); r = row of the pair's first row relative to vlo (-1 when
+  // vlo is odd: that row is outside the box and carries E = 0)
 #pragma unroll 1
-  for (int r2 = 0; r2 < ht; r2 += 2) {
-    const bool vB = r2 + 1 < ht;
-    const float dyA = dy0 + (float)r2, dyB = dyA + 1.f;
-    const float *ga = gi + (size_t)r2 * c.D, *gb = ga + c.D;
+  for (int r = -(vlo & 1); r < ht; r += 2) {
+    const bool vA = r >= 0, vB = r + 1 < ht;
+    const float dyA = dy0 + (float)r, dyB = dyA + 1.f;
+    const float2 *gp = reinterpret_cast<const float2 *>(gi) + (size_t)((r + (vlo & 1)) >> 1) * c.D;
     float2 C = make_float2(0.f, 0.f), Q = C, Z = C;
     if (!slow) {
       float2 E2, R2;
-      E2.x = El;
-      R2.x = Rl;
-      El *= V; V *= W; Rl *= Kb;
+      E2.x = vA ? El : 0.f;
+      R2.x = vA ? Rl : 0.f;
+      if (vA) { El *= V; V *= W; Rl *= Kb; }
       E2.y = vB ? El : 0.f;
       R2.y = vB ? Rl : 0.f;
       if (vB) { El *= V; V *= W; Rl *= Kb; }
-      // column pairs at even absolute columns are read with one 64-bit load per row (half the
-      // L1 requests); an odd first column and an odd last column are peeled
+      // column pairs at even absolute columns are read with one 128-bit load (two columns of the
+      // row pair); an odd first column and an odd last column are peeled
       int k = 0;
-      auto step = [&](float gA, float gBv) {
+      auto step = [&](float2 g2) {
         const float2 Em = MK ? make_float2(E2.x >= ethr ? E2.x : 0.f, E2.y >= ethr ? E2.y : 0.f) : E2;
-        C = __ffma2_rn(make_float2(gA, gBv), Em, C);   // C += h, h = g e
+        C = __ffma2_rn(g2, Em, C);   // C += h, h = g e
         Q = __fadd2_rn(Q, C);
         Z = __fadd2_rn(Z, Q);
         E2 = __fmul2_rn(E2, R2);
         R2 = __fmul2_rn(R2, S2);
       };
       if (ulo & 1) {
-        step(__ldg(ga), vB ? __ldg(gb) : 0.f);
+        step(__ldg(gp));
         k = 1;
       }
 #pragma unroll 1
       for (; k + 1 < wd; k += 2) {
-        const float2 a2 = __ldg(reinterpret_cast<const float2 *>(ga + k));
-        const float2 b2 = vB ? __ldg(reinterpret_cast<const float2 *>(gb + k)) : make_float2(0.f, 0.f);
-        step(a2.x, b2.x);
-        step(a2.y, b2.y);
+        const float4 g4 = __ldg(reinterpret_cast<const float4 *>(gp + k));
+        step(make_float2(g4.x, g4.y));
+        step(make_float2(g4.z, g4.w));
       }
-      if (k < wd) step(__ldg(ga + k), vB ? __ldg(gb + k) : 0.f);
+      if (k < wd) step(__ldg(gp + k));
     } else {   // direct evaluation, exp per pixel; sums converted to (C, Q, Z) form
       const float fA = fmaf(dyA, fmaf(nc, dyA, Gx), Fx), fB = fmaf(dyB, fmaf(nc, dyB, Gx), Fx);
       const float gA = fmaf(nb2, dyA, D0), gB = fmaf(nb2, dyB, D0);
@@ -539,8 +541,9 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const
         const float tf = wf - (float)k, kf = (float)k, kq = kf * (kf - 1.f) * na;
         float eA = ex2(fmaf(kf, gA, fA) + kq), eB = ex2(fmaf(kf, gB, fB) + kq);
         if (MK) { eA = eA >= ethr ? eA : 0.f; eB = eB >= ethr ? eB : 0.f; }
-        const float hA = __ldg(ga + k) * eA;
-        const float hB = vB ? __ldg(gb + k) * eB : 0.f;
+        const float2 g2 = __ldg(gp + k);
+        const float hA = vA ? g2.x * eA : 0.f;
+        const float hB = vB ? g2.y * eB : 0.f;
         const float zt = 0.5f * tf * (tf + 1.f);
         C.x += hA; C.y += hB;
         Q.x = fmaf(hA, tf, Q.x); Q.y = fmaf(hB, tf, Q.y);
@@ -590,6 +593,19 @@ __global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const
   float *dst = slots + (size_t)chunk * 10 * c.N + j;
 #pragma unroll
   for (int k = 0; k < 10; ++k) dst[(size_t)k * c.N] = vacc[k];
+}
+
+// dL/dI (B images of D x D, row-major, from the C2R) -> row-pair interleaved layout read by
+// k_render_bwd: out[i][m][u] = (g[i][2m][u], g[i][2m + 1][u]) (D even)
+__global__ void __launch_bounds__(256) k_dldi_pack(int D, int64_t npairs, const float2 *__restrict__ in,
+                                                   float4 *__restrict__ out) {
+  const int h = D >> 1;   // column pairs per row
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (pair row, column pair)
+  if (t >= npairs * h) return;
+  const int64_t pr = t / h;
+  const int64_t src = 2 * pr * h + (t - pr * h);
+  const float2 a = __ldcs(in + src), b = __ldcs(in + src + h);
+  out[t] = make_float4(a.x, b.x, a.y, b.y);
 }
 
 // Per-Gaussian reduction of the chunk slots in chunk order (deterministic), added to acc:
@@ -651,6 +667,13 @@ void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *b
     if (mk) launch_fwd_t<16, true>(c, B, rec, base, ids, proj, ticket, s);
     else launch_fwd_t<16, false>(c, B, rec, base, ids, proj, ticket, s);
   }
+  ++launches;
+}
+
+void launch_dldi_pack(const CfgDev &c, int B, const float *in, float *out, cudaStream_t s, int &launches) {
+  const int64_t np = (int64_t)B * c.D / 2, n = np * c.D;
+  k_dldi_pack<<<(unsigned)((n / 2 + 255) / 256), 256, 0, s>>>(c.D, np, reinterpret_cast<const float2 *>(in),
+                                                              reinterpret_cast<float4 *>(out));
   ++launches;
 }
 
