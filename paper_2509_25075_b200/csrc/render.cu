@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
 constexpr int kBwdBlock = 256, kBwdP = 8;   // threads per block, particles per thread
 
 template <bool MK>
-__global__ void __launch_bounds__(kBwdBlock) k_render_bwd(CfgDev c, int B, const SplatRec *__restrict__ rec,
+__global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, const SplatRec *__restrict__ rec,
                                                           const float *__restrict__ dldi,
                                                           const float *__restrict__ rot, float *__restrict__ slots) {
   constexpr float nh = -0.5f * kLog2e;
