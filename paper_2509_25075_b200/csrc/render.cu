@@ -527,10 +527,19 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
         k = 1;
       }
 #pragma unroll 1
-      for (; k + 1 < wd; k += 2) {
+      for (; k + 3 < wd; k += 4) {   // two 128-bit loads in flight
+        const float4 g4 = __ldg(reinterpret_cast<const float4 *>(gp + k));
+        const float4 h4 = __ldg(reinterpret_cast<const float4 *>(gp + k + 2));
+        step(make_float2(g4.x, g4.y));
+        step(make_float2(g4.z, g4.w));
+        step(make_float2(h4.x, h4.y));
+        step(make_float2(h4.z, h4.w));
+      }
+      if (k + 1 < wd) {
         const float4 g4 = __ldg(reinterpret_cast<const float4 *>(gp + k));
         step(make_float2(g4.x, g4.y));
         step(make_float2(g4.z, g4.w));
+        k += 2;
       }
       if (k < wd) step(__ldg(gp + k));
     } else {   // direct evaluation, exp per pixel; sums converted to (C, Q, Z) form
