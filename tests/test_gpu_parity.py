@@ -580,13 +580,15 @@ def test_negative_densities(gem, orc, tile):
         assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
 
 
-@pytest.mark.parametrize("D", [64, 48])
+@pytest.mark.parametrize("D", [64, 128, 256, 48])
 def test_spectral_paths(gem, orc, D):
-    """The row-column spectral path (D = 64: cuFFT 1D rows + k_ctf_colspec<8, 8>) and the 2D
-    fallback (D = 48: 2D cuFFT + k_ctf_loss) against the oracle: images, prediction, loss and
-    gradients."""
+    """The row-column spectral path (D = 64 / 128 / 256: cuFFT 1D rows + k_ctf_colspec<8, 8> /
+    <16, 8> / <16, 16>, whose packed gradient rows Z = A + iB take the in-lane (S = 2) and the
+    cross-lane (S = 1) pairing) and the 2D fallback (D = 48: 2D cuFFT + k_ctf_loss +
+    k_dldi_pack) against the oracle: images, prediction, loss and gradients."""
     case = make_case("T", B=3, seed=29, N=800, D=D)
-    g = run_gpu(gem, case)
+    g = run_gpu(gem, case, cap=1 << 18)   # the default list capacity is sized for N, not for D
+    assert g["stats"]["overflow"] == 0
     o = oracle_out(orc, case)
     for i in range(3):
         assert maxnorm_rel(g["proj"][i], o["proj"][i]) < IMG_TOL
