@@ -80,11 +80,16 @@ SHAPES = {"T": "tiny synthetic", "S": "CryoBench-like small protein", "R": "EMPI
           "P": "EMPIAR-10180-shaped spliceosome", "X": "large-scale stress", "A": "desk-scale round trip"}
 
 
-def measured_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (profiles/traffic.json)."""
+def measured_traffic(kernel, workload, batch, tile, variant):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    (profiles/traffic.json); None unless this run has the captured configuration."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(p))[kernel]["dram_bytes_per_launch"]
+        t = json.load(open(p))
+        cap = t["config"]
+        if (workload, batch, tile, variant) != (cap["workload"], cap["batch"], cap["tile"], cap["variant"]):
+            return None
+        return t[kernel]["dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -369,6 +374,8 @@ def main():
     kernels = {k: {"ms_per_step": v[1] / max(args.steps, 1), "launch_groups": v[0],
                    "share": v[1] / total_kernel_ms if total_kernel_ms else None} for k, v in kern.items()}
     pairs = int(st["pairs"])
+    variant = (f"{args.state}|fused={args.fused}|zsort={args.zsort}|mask={args.pixel_mask}"
+               f"|exact={args.exact_tiles}")
     dominant = max(kern, key=lambda k: kern[k][1]) if kern else None
     roof = None
     if dominant in ("render_fwd", "render_bwd"):
@@ -377,7 +384,8 @@ def main():
         achieved = per_pair * pairs * args.steps / (kern[dominant][1] / 1e3) / 1e12
         peak = fp32_peak_tflops(sm_max)
         roof = {"bound": "alu", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": measured_traffic(dominant),
+                "frac": achieved / peak,
+                "traffic": measured_traffic(dominant, args.config, B, args.tile, variant),
                 "work_per_launch": f"{per_pair} FP32 FLOP x {pairs} useful (Gaussian, pixel) pairs per step, "
                                    f"{kern[dominant][0] // max(args.steps, 1)} launch(es) per step",
                 "avg_launch_ms": avg_s * 1e3,
