@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--global-batch", type=int, default=0,
                     help="strong scaling: this many particles per step in total, split over the GPUs")
     ap.add_argument("--zsort", action="store_true", help="P:227 z-sorted tile lists (GEM_FLAG_ZSORT)")
+    ap.add_argument("--no-volume", action="store_true", help="skip the gem_render_volume timing (row a11)")
     ap.add_argument("--pixel-mask", default="aabb", choices=["aabb", "ellipse", "tau", "ellipse+tau"],
                     help="Eq. 8 per-pixel selection variant (GEM_FLAG_ELLIPSE / GEM_FLAG_PIXEL_TAU)")
     ap.add_argument("--tau", type=float, default=0.0)
@@ -406,6 +407,37 @@ def main():
                  "model": "31 FP32 lane-ops per useful pair at 148 SM x 128 lanes x f_max + cuFFT/CTF chain "
                           "bytes at the measured HBM copy bandwidth (SURVEY 8(d))"}
 
+    # §8(a) row a11: the volume query gem_render_volume at Dv = D on the trained model, timed
+    # outside the step (CUDA events on the library's stream, 2 warm-up + 5 timed calls); its
+    # algorithmic traffic is the 4 Dv^3 bytes of the volume written once
+    vol = None
+    if not args.no_volume:
+        Dv = w.D
+        vout = torch.empty((Dv, Dv, Dv), dtype=torch.float32, device=dev)
+        for _ in range(2):
+            sc.render_volume(tr.params, Dv, px, out=vout)
+        vs = sc.stream
+        ve0, ve1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        l0 = sc.launches
+        sc.profile(True)
+        ve0.record(vs)
+        for _ in range(5):
+            sc.render_volume(tr.params, Dv, px, out=vout)
+        ve1.record(vs)
+        torch.cuda.synchronize()
+        sc.profile(False)
+        vdev = sc.profile_read().get("volume", (0, 0.0))
+        vms = vdev[1] / max(vdev[0], 1)   # device time per call (event pair around its launches)
+        hbm = float(peaks.get("hbm_gbs", 6537.6))
+        vol = {"Dv": Dv, "voxel_A": px, "ms": vms, "ms_per_call_with_host_sync": ve0.elapsed_time(ve1) / 5,
+               "achieved_gbs": 4.0 * Dv ** 3 / (vms * 1e-3) / 1e9, "peak_gbs": hbm,
+               "frac": 4.0 * Dv ** 3 / (vms * 1e-3) / 1e9 / hbm, "bound": "issue (the per-hit brick loop); frac is against the HBM floor of the 4 Dv^3 B write",
+               "gpu_launches_per_call": (sc.launches - l0) / 5,
+               "includes": "brick count, scan, brick-list fill and the per-brick render; the call's overflow "
+                           "check (a 24 B D2H + stream sync) only in ms_per_call_with_host_sync"}
+        del vout
+
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -429,7 +461,7 @@ def main():
                    "useful_pairs_per_step": pairs, "list_entries_per_step": int(st["entries"])},
         "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks,
-        "memory": memory, "replicas_identical": replicas,
+        "memory": memory, "replicas_identical": replicas, "volume": vol,
         "kernels": kernels,
         "kernel_times": "CUDA event pair around each launch group, second pass over the same K steps",
     }

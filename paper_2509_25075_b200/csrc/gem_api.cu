@@ -588,12 +588,20 @@ gem_status gem_render_volume(gem_ctx *ctx, const gem_soa *params, int32_t Dv, fl
   cudaStream_t s = (cudaStream_t)stream;
   ctx->stream = s;
   ctx->launches = 0;
-  Prof pv(ctx, s, P_VOLUME);
-  cudaError_t e = launch_volume(ctx->dc.N, (const float4 *)params->mean_rho, (const float4 *)params->log_scale,
-                                (const float4 *)params->quat, Dv, voxel_size, ctx->cfg.cull_k, vol_out, sc,
-                                scratch_bytes, s, ctx->launches);
-  if (e == cudaErrorInvalidValue) return GEM_E_CAPACITY;
+  DevStats *dst = nullptr;
+  cudaError_t e;
+  {
+    Prof pv(ctx, s, P_VOLUME);   // device time of the query (the overflow check below syncs)
+    e = launch_volume(ctx->dc.N, (const float4 *)params->mean_rho, (const float4 *)params->log_scale,
+                      (const float4 *)params->quat, Dv, voxel_size, ctx->cfg.cull_k, vol_out, sc, scratch_bytes, s,
+                      ctx->launches, &dst);
+  }
   if (e != cudaSuccess) return GEM_E_CUDA;
+  DevStats h;
+  if (cudaMemcpyAsync(&h, dst, sizeof(DevStats), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return GEM_E_CUDA;
+  if (h.overflow) return GEM_E_CAPACITY;
   return GEM_OK;
 }
 

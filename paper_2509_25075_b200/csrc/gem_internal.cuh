@@ -202,5 +202,5 @@ void launch_adam(int N, float4 *p_mr, float4 *p_ls, float4 *p_q, const float4 *g
 size_t volume_scratch_bytes(int N, int Dv);
 cudaError_t launch_volume(int N, const float4 *mean_rho, const float4 *log_scale, const float4 *quat, int Dv,
                           float vs, float k, float *vol, char *scratch, size_t scratch_bytes, cudaStream_t s,
-                          int &launches);
+                          int &launches, DevStats **st_out);
 }  // namespace gem

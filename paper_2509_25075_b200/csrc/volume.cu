@@ -111,7 +111,9 @@ __global__ void __launch_bounds__(256) k_vol_fill(int N, const VolRec *__restric
       }
 }
 
-// One CTA per 8^3 brick, 512 threads (one voxel each); warp = 8x4x1 voxels.
+// Persistent CTAs of 512 threads (one voxel each; warp = 8x4x1 voxels), each walking 8^3 bricks
+// b = blockIdx.x, + gridDim.x, ...; empty bricks (most of a Dv^3 grid) are skipped: the volume
+// is zeroed by a memset first.
 __global__ void __launch_bounds__(512) k_vol_render(const VolRec *__restrict__ rec, const int *__restrict__ off,
                                                     const int *__restrict__ ids, int64_t cap, int Dv, float vs, int nb,
                                                     float *__restrict__ vol) {
@@ -119,7 +121,10 @@ __global__ void __launch_bounds__(512) k_vol_render(const VolRec *__restrict__ r
   __shared__ float4 sb[512];   // inv00 inv01 inv02 inv11 (scaled by -1/2 log2e)
   __shared__ float2 sc[512];   // inv12 inv22
   __shared__ int4 sbox[512];   // brick-local (xlo, xhi, ylo|yhi<<16, zlo|zhi<<16)
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nbr = nb * nb * nb;
+  for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+  if (off[b] >= off[b + 1] || (int64_t)off[b] >= cap) continue;   // empty brick: zeros (memset)
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int bx = b % nb, by = (b / nb) % nb, bz = b / (nb * nb);
   const int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
   const int lx = lane & 7, ly = (w & 1) * 4 + (lane >> 3), lz = w >> 1;
@@ -182,6 +187,8 @@ __global__ void __launch_bounds__(512) k_vol_render(const VolRec *__restrict__ r
   }
   const int X = x0 + lx, Y = y0 + ly, Z = z0 + lz;
   if (X < Dv && Y < Dv && Z < Dv) vol[((size_t)Z * Dv + Y) * Dv + X] = acc;
+  __syncthreads();   // the next brick's staging overwrites the shared lists
+  }
 }
 
 }  // namespace
@@ -202,9 +209,10 @@ size_t volume_scratch_bytes(int N, int Dv) {
 void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, DevStats *st, int64_t cap, cudaStream_t s,
                  int &launches);
 
+// Enqueues the query; *st_out receives the device counters (overflow) for the caller's check.
 cudaError_t launch_volume(int N, const float4 *mean_rho, const float4 *log_scale, const float4 *quat, int Dv,
                           float vs, float k, float *vol, char *scratch, size_t scratch_bytes, cudaStream_t s,
-                          int &launches) {
+                          int &launches, DevStats **st_out) {
   const int nb = (Dv + kBrick - 1) / kBrick;
   const size_t nbr = (size_t)nb * nb * nb;
   const size_t nblk = (nbr + 1 + 4095) / 4096;
@@ -223,14 +231,19 @@ cudaError_t launch_volume(int N, const float4 *mean_rho, const float4 *log_scale
   k_vol_prep<<<(N + 255) / 256, 256, 0, s>>>(N, mean_rho, log_scale, quat, Dv, (double)vs, (double)k, rec, cnt, nb);
   launch_scan(cnt, off, (int64_t)nbr, blk, (int64_t)nblk, st, cap, s, launches);
   k_vol_fill<<<(N + 255) / 256, 256, 0, s>>>(N, rec, off, cur, ids, cap, nb);
-  k_vol_render<<<(unsigned)nbr, 512, 0, s>>>(rec, off, ids, cap, Dv, vs, nb, vol);
+  static int rgrid = 0;
+  if (!rgrid) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vol_render, 512, 0);
+    rgrid = (sms > 0 ? sms : 148) * (per > 0 ? per : 1);
+  }
+  const unsigned g = (unsigned)(nbr < (size_t)rgrid ? nbr : (size_t)rgrid);
+  cudaMemsetAsync(vol, 0, sizeof(float) * (size_t)Dv * Dv * Dv, s);
+  k_vol_render<<<g, 512, 0, s>>>(rec, off, ids, cap, Dv, vs, nb, vol);
   launches += 3;
-  DevStats h;
-  cudaError_t err = cudaMemcpyAsync(&h, st, sizeof(DevStats), cudaMemcpyDeviceToHost, s);
-  if (err != cudaSuccess) return err;
-  err = cudaStreamSynchronize(s);
-  if (err != cudaSuccess) return err;
-  if (h.overflow) return cudaErrorInvalidValue;  // mapped to GEM_E_CAPACITY by the caller
+  *st_out = st;
   return cudaGetLastError();
 }
 
