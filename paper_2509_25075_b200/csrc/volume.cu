@@ -111,83 +111,115 @@ __global__ void __launch_bounds__(256) k_vol_fill(int N, const VolRec *__restric
       }
 }
 
-// Persistent CTAs of 512 threads (one voxel each; warp = 8x4x1 voxels), each walking 8^3 bricks
-// b = blockIdx.x, + gridDim.x, ...; empty bricks (most of a Dv^3 grid) are skipped: the volume
-// is zeroed by a memset first.
-__global__ void __launch_bounds__(512) k_vol_render(const VolRec *__restrict__ rec, const int *__restrict__ off,
-                                                    const int *__restrict__ ids, int64_t cap, int Dv, float vs, int nb,
-                                                    float *__restrict__ vol) {
-  __shared__ float4 sa[512];   // mu (voxel-local, in Angstrom), rho
-  __shared__ float4 sb[512];   // inv00 inv01 inv02 inv11 (scaled by -1/2 log2e)
-  __shared__ float2 sc[512];   // inv12 inv22
-  __shared__ int4 sbox[512];   // brick-local (xlo, xhi, ylo|yhi<<16, zlo|zhi<<16)
+// Persistent CTAs of 64 threads, each walking the non-empty 8^3 bricks b = blockIdx.x,
+// + gridDim.x, ... (the volume is zeroed by a memset first; most bricks of a Dv^3 grid are
+// empty).  Thread (lx, ly) owns the brick's voxel column (x0 + lx, y0 + ly, z0 .. z0 + 7); warp w
+// the rows ly in [4w, 4w + 4).  A brick's entries are staged in shared memory 64 at a time; per
+// 32 entries each lane tests one against its warp's 8 x 4 x 8 slab, and the warp walks the hits
+// (ballot).  Along z the log2-kernel is quadratic, q(dz) = q_xy + (L + F dz) dz, so a column is
+// evaluated by the render's multiplicative recurrence, e <- e r, r <- r s (s = 2^{2F}): 2 exps and
+// ~3 instructions per voxel instead of an exp per voxel; entries whose start values leave the
+// normal range take the direct path.
+constexpr int kVolThreads = 64;
+
+__global__ void __launch_bounds__(kVolThreads) k_vol_render(const VolRec *__restrict__ rec, const int *__restrict__ off,
+                                                            const int *__restrict__ ids, int64_t cap, int Dv, float vs,
+                                                            int nb, float *__restrict__ vol) {
+  __shared__ float4 sa[kVolThreads];   // centre (voxel units, brick-local), rho
+  __shared__ float4 sb[kVolThreads];   // A, 2B, 2C, D of q (Sigma^-1 in voxel units, x -1/2 log2 e)
+  __shared__ float4 sc[kVolThreads];   // 2E, F, s = 2^{2F}, -
+  __shared__ int4 sbox[kVolThreads];   // brick-local x lo|hi<<16, y lo|hi<<16, z lo|hi<<16, -
   const int nbr = nb * nb * nb;
-  for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
-  if (off[b] >= off[b + 1] || (int64_t)off[b] >= cap) continue;   // empty brick: zeros (memset)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int bx = b % nb, by = (b / nb) % nb, bz = b / (nb * nb);
-  const int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
-  const int lx = lane & 7, ly = (w & 1) * 4 + (lane >> 3), lz = w >> 1;
-  const int wy0 = (w & 1) * 4, wz = w >> 1;
+  const int lx = tid & 7, ly = tid >> 3, wy0 = 4 * w;
   const double half = (double)(Dv / 2);
-  // voxel-local coordinates (voxel units) relative to the brick origin voxel
-  const float rx = (float)lx, ry = (float)ly, rz = (float)lz;
-  const float vs2 = vs * vs;
-  int s = off[b], e = off[b + 1];
-  if ((int64_t)e > cap) e = (int)cap;
-  if ((int64_t)s > cap) s = (int)cap;
-  float acc = 0.f;
-  const float nh = -0.5f * kLog2e;
-  for (int cs = s; cs < e; cs += 512) {
-    const int n = min(512, e - cs);
-    __syncthreads();
-    if (tid < n) {
-      const VolRec r = rec[ids[cs + tid]];
-      // centre in voxel units relative to voxel (x0, y0, z0), rounded once from fp64
-      sa[tid] = make_float4((float)((double)r.a.x / vs + half - x0), (float)((double)r.a.y / vs + half - y0),
-                            (float)((double)r.a.z / vs + half - z0), r.a.w);
-      const float sc2 = nh * vs2;   // Sigma^-1 in voxel units, prescaled by -1/2 log2e
-      sb[tid] = make_float4(sc2 * r.b.x, 2.f * sc2 * r.b.y, 2.f * sc2 * r.b.z, sc2 * r.b.w);
-      sc[tid] = make_float2(2.f * sc2 * r.c.x, sc2 * r.c.y);
-      const int px_ = __float_as_int(r.c.z), py_ = __float_as_int(r.c.w), pz_ = r.d.x;
-      const int xl = (px_ & 0xffff) - x0, xh = (px_ >> 16) - x0;
-      const int yl = (py_ & 0xffff) - y0, yh = (py_ >> 16) - y0;
-      const int zl = (pz_ & 0xffff) - z0, zh = (pz_ >> 16) - z0;
-      auto cl = [](int v) { return v < -1 ? -1 : (v > 8 ? 8 : v); };
-      sbox[tid] = make_int4((cl(xl) & 0xffff) | (cl(xh) << 16), 0, (cl(yl) & 0xffff) | (cl(yh) << 16), (cl(zl) & 0xffff) | (cl(zh) << 16));
-    }
-    __syncthreads();
-    for (int g = 0; g < n; g += 32) {
-      const int k = g + lane;
-      bool hit = false;
-      if (k < n) {
-        const int4 bb = sbox[k];
-        const int xl = (short)(bb.x & 0xffff), xh = bb.x >> 16, yl = (short)(bb.z & 0xffff), yh = bb.z >> 16;
-        const int zl = (short)(bb.w & 0xffff), zh = bb.w >> 16;
-        hit = xl <= 7 && xh >= 0 && yl <= wy0 + 3 && yh >= wy0 && zl <= wz && zh >= wz;
+  const float sc2 = -0.5f * kLog2e * vs * vs;
+  const float rx = (float)lx, ry = (float)ly;
+  for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+    int s = off[b], e = off[b + 1];
+    if ((int64_t)e > cap) e = (int)cap;
+    if (s >= e) continue;   // empty brick: zeros (memset)
+    const int bx = b % nb, by = (b / nb) % nb, bz = b / (nb * nb);
+    const int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
+    float acc[kBrick];
+#pragma unroll
+    for (int z = 0; z < kBrick; ++z) acc[z] = 0.f;
+    for (int cs = s; cs < e; cs += kVolThreads) {
+      const int n = min(kVolThreads, e - cs);
+      __syncthreads();
+      if (tid < n) {
+        const VolRec r = rec[ids[cs + tid]];
+        // centre in voxel units relative to voxel (x0, y0, z0), rounded once from fp64
+        sa[tid] = make_float4((float)((double)r.a.x / vs + half - x0), (float)((double)r.a.y / vs + half - y0),
+                              (float)((double)r.a.z / vs + half - z0), r.a.w);
+        const float F = sc2 * r.c.y;
+        sb[tid] = make_float4(sc2 * r.b.x, 2.f * sc2 * r.b.y, 2.f * sc2 * r.b.z, sc2 * r.b.w);
+        float s2;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(s2) : "f"(2.f * F));
+        sc[tid] = make_float4(2.f * sc2 * r.c.x, F, s2, 0.f);
+        const int px_ = __float_as_int(r.c.z), py_ = __float_as_int(r.c.w), pz_ = r.d.x;
+        auto cl = [](int v) { return v < -1 ? -1 : (v > 8 ? 8 : v); };
+        const int xl = cl((px_ & 0xffff) - x0), xh = cl((px_ >> 16) - x0);
+        const int yl = cl((py_ & 0xffff) - y0), yh = cl((py_ >> 16) - y0);
+        const int zl = cl((pz_ & 0xffff) - z0), zh = cl((pz_ >> 16) - z0);
+        sbox[tid] = make_int4((xl & 0xffff) | (xh << 16), (yl & 0xffff) | (yh << 16), (zl & 0xffff) | (zh << 16), 0);
       }
-      unsigned m = __ballot_sync(0xffffffffu, hit);
-      while (m) {
-        const int kk = g + __ffs(m) - 1;
-        m &= m - 1;
-        const int4 bb = sbox[kk];
-        const int xl = (short)(bb.x & 0xffff), xh = bb.x >> 16, yl = (short)(bb.z & 0xffff), yh = bb.z >> 16;
-        const int zl = (short)(bb.w & 0xffff), zh = bb.w >> 16;
-        const bool inside = lx >= xl && lx <= xh && ly >= yl && ly <= yh && lz >= zl && lz <= zh;
-        const float4 A = sa[kk], Bv = sb[kk];
-        const float2 Cv = sc[kk];
-        const float dx = rx - A.x, dy = ry - A.y, dz = rz - A.z;
-        // q = -1/2 log2e d^T inv d
-        const float qv = dx * fmaf(Bv.x, dx, fmaf(Bv.y, dy, Bv.z * dz)) + dy * fmaf(Bv.w, dy, Cv.x * dz) + Cv.y * dz * dz;
-        float ev;
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ev) : "f"(qv));
-        if (inside) acc = fmaf(A.w, ev, acc);
+      __syncthreads();
+      for (int g = 0; g < n; g += 32) {
+        const int k = g + lane;
+        bool hit = false;
+        if (k < n) {
+          const int4 bb = sbox[k];
+          const int xl = (short)(bb.x & 0xffff), xh = bb.x >> 16, yl = (short)(bb.y & 0xffff), yh = bb.y >> 16;
+          const int zl = (short)(bb.z & 0xffff), zh = bb.z >> 16;
+          hit = xl <= 7 && xh >= 0 && yl <= wy0 + 3 && yh >= wy0 && zl <= 7 && zh >= 0;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, hit);
+        while (m) {
+          const int kk = g + __ffs(m) - 1;
+          m &= m - 1;
+          const int4 bb = sbox[kk];
+          const int xl = (short)(bb.x & 0xffff), xh = bb.x >> 16, yl = (short)(bb.y & 0xffff), yh = bb.y >> 16;
+          if (!(lx >= xl && lx <= xh && ly >= yl && ly <= yh)) continue;
+          const int za = max((int)(short)(bb.z & 0xffff), 0), zb = min(bb.z >> 16, 7);
+          const float4 A = sa[kk], Bq = sb[kk], Cq = sc[kk];
+          const float dx = rx - A.x, dy = ry - A.y, dz0 = (float)za - A.z;
+          const float qxy = fmaf(dx, fmaf(Bq.x, dx, Bq.y * dy), Bq.w * dy * dy);
+          const float L = fmaf(Bq.z, dx, Cq.x * dy), F = Cq.y;
+          const float q0 = fmaf(dz0, fmaf(F, dz0, L), qxy), r0 = fmaf(F, fmaf(2.f, dz0, 1.f), L);
+          if (q0 >= -100.f && r0 >= -120.f && F >= -60.f) {
+            float ev, rv;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ev) : "f"(q0));
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(rv) : "f"(r0));
+            ev *= A.w;
+#pragma unroll
+            for (int z = 0; z < kBrick; ++z) {
+              if (z >= za && z <= zb) {
+                acc[z] += ev;
+                ev *= rv;
+                rv *= Cq.z;
+              }
+            }
+          } else {   // direct evaluation
+#pragma unroll
+            for (int z = 0; z < kBrick; ++z) {
+              if (z >= za && z <= zb) {
+                const float dz = (float)z - A.z;
+                float ev;
+                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ev) : "f"(fmaf(dz, fmaf(F, dz, L), qxy)));
+                acc[z] = fmaf(A.w, ev, acc[z]);
+              }
+            }
+          }
+        }
       }
     }
-  }
-  const int X = x0 + lx, Y = y0 + ly, Z = z0 + lz;
-  if (X < Dv && Y < Dv && Z < Dv) vol[((size_t)Z * Dv + Y) * Dv + X] = acc;
-  __syncthreads();   // the next brick's staging overwrites the shared lists
+    const int X = x0 + lx, Y = y0 + ly;
+    if (X < Dv && Y < Dv) {
+#pragma unroll
+      for (int z = 0; z < kBrick; ++z)
+        if (z0 + z < Dv) vol[((size_t)(z0 + z) * Dv + Y) * Dv + X] = acc[z];
+    }
   }
 }
 
@@ -236,12 +268,12 @@ cudaError_t launch_volume(int N, const float4 *mean_rho, const float4 *log_scale
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vol_render, 512, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vol_render, kVolThreads, 0);
     rgrid = (sms > 0 ? sms : 148) * (per > 0 ? per : 1);
   }
   const unsigned g = (unsigned)(nbr < (size_t)rgrid ? nbr : (size_t)rgrid);
   cudaMemsetAsync(vol, 0, sizeof(float) * (size_t)Dv * Dv * Dv, s);
-  k_vol_render<<<g, 512, 0, s>>>(rec, off, ids, cap, Dv, vs, nb, vol);
+  k_vol_render<<<g, kVolThreads, 0, s>>>(rec, off, ids, cap, Dv, vs, nb, vol);
   launches += 3;
   *st_out = st;
   return cudaGetLastError();

@@ -238,6 +238,27 @@ def test_render_volume(gem, orc):
     assert maxnorm_rel(vol2, ref2) < IMG_TOL
 
 
+@pytest.mark.parametrize("stretch", [False, True])
+def test_render_volume_bricks(gem, orc, stretch):
+    """Volume query over many 8^3 bricks (Dv = 48 and a ragged 45): boxes spanning several
+    bricks, the z-column recurrence and, with needle-like Gaussians (one axis x e^1.5, one
+    x e^-1), its direct-evaluation path."""
+    case = make_case("T", B=1, seed=31, N=1500, D=48)
+    mr, ls, q = case["params"]
+    if stretch:
+        ls = ls.copy()
+        ls[:, 0] += 1.5
+        ls[:, 1] -= 1.0
+    w = case["w"]
+    vs = float(np.float32(w.px))
+    st = gem.GemStep(gem.GemConfig(D=w.D, pixel_size=vs, n_gauss=w.N, max_batch=1))
+    P = gem.SoA.from_arrays(mr, ls, q, device=st.device)
+    for Dv in (48, 45):
+        vol = st.render_volume(P, Dv, vs).cpu().numpy()
+        ref = orc.volume((mr, ls, q), Dv, vs, masked=True)
+        assert maxnorm_rel(vol, ref) < IMG_TOL, Dv
+
+
 def test_empty_lists_all_offframe(gem):
     case = make_case("T", B=2, seed=9)
     mr = case["params"][0].copy()
