@@ -12,7 +12,7 @@ timeout 900 python -m pytest tests -m gpu -q > gpurun_out/round/pytest_gpu.log 2
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/round/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/round/smoke.log
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/round/bench_$TAG.json 2> gpurun_out/round/bench_$TAG.err; echo "bench rc=$?" >> gpurun_out/round/bench_$TAG.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/round/bench_ref_$TAG.json 2> gpurun_out/round/bench_ref_$TAG.err
-CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-volume"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/round/launches_$TAG.csv $CMD > gpurun_out/round/ncu_launch.log 2>&1
 # skip the observation generator's forwards (ring 1024 / batch) and the warm-up step
 FSKIP=$(( 1024 / ${BATCH:-256} + 1 ))
