@@ -145,7 +145,8 @@ typedef struct {
   int64_t entries;        /* (Gaussian, tile) list entries of the last gem_forward           */
   int64_t capacity;       /* list_capacity in use                                          */
   int32_t degenerate;     /* Gaussians with |q| = 0 or non-finite prep in the last forward  */
-  int32_t overflow;       /* 1 if entries > capacity in the last forward                     */
+  int32_t overflow;       /* 1 if entries > capacity in any forward since the previous
+                             gem_stats call (sticky; cleared by this call)                   */
   int32_t nonfinite;      /* 1 if a non-finite loss or gradient was produced                 */
   int32_t batch;          /* B of the last gem_forward                                       */
   int64_t workspace_bytes;

@@ -659,6 +659,11 @@ gem_status gem_stats(gem_ctx *ctx, gem_stats_t *out) {
   CK(cudaStreamSynchronize(ctx->stream));
   DevStats h;
   CK(cudaMemcpy(&h, ctx->ws + ctx->L.stats, sizeof(DevStats), cudaMemcpyDeviceToHost));
+  // sticky overflow word (ticket[12], set by the scan of any forward since the last call)
+  int sticky = 0;
+  CK(cudaMemcpy(&sticky, ctx->ws + ctx->L.ticket + 12 * sizeof(int), sizeof(int), cudaMemcpyDeviceToHost));
+  if (sticky) CK(cudaMemset(ctx->ws + ctx->L.ticket + 12 * sizeof(int), 0, sizeof(int)));
+  h.overflow |= sticky;
   out->entries = (int64_t)h.entries;
   out->capacity = ctx->dc.cap;
   out->degenerate = h.degenerate;

@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(k1pThreads) k_scan_1p(const int *__restrict__ 
       const int tot = s_prefix + total;
       out[n] = tot;
       st->entries += (unsigned long long)tot;
-      if ((int64_t)tot > cap) st->overflow = 1;
+      if ((int64_t)tot > cap) { st->overflow = 1; tk[4] = 1; }   // tk[4]: sticky until gem_stats
     }
     __threadfence();
     if (atomicAdd(tk + 1, 1) == (int)nblk - 1) { tk[0] = 0; tk[1] = 0; }

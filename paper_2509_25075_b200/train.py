@@ -55,6 +55,7 @@ def fit(trainer, data: dict, epochs: int, batch: int, seed: int = 0, start_epoch
         history.append(float(tot) / n)
         if not np.isfinite(history[-1]):
             raise FloatingPointError(f"non-finite loss in epoch {ep}")
+        trainer.step_ctx.stats(check=True)   # raises if any step's tile lists overflowed (sticky flag)
         if checkpoint and checkpoint_every and (ep + 1) % checkpoint_every == 0:
             save_checkpoint(checkpoint, trainer.params.t, trainer.m.t, trainer.v.t, trainer.t, ep + 1)
     return history

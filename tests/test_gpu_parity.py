@@ -289,6 +289,17 @@ def test_errors_and_capacity(gem):
     st.forward(P, t(case["rot"][:1]), t(case["shift"][:1]), t(case["ctf"][:1]), t(case["obs"][:1]))
     s = st.stats(check=False)
     assert s["status"] == b.GEM_E_CAPACITY and s["overflow"] == 1 and s["entries"] > 10
+    # the overflow flag is sticky across forwards until gem_stats reads it: an overflowing
+    # forward followed by one that fits (all Gaussians off-frame) still reports it once
+    st.forward(P, t(case["rot"][:1]), t(case["shift"][:1]), t(case["ctf"][:1]), t(case["obs"][:1]))
+    mr_off = case["params"][0].copy()
+    mr_off[:, :3] += 1e5
+    P_off = gem.SoA.from_arrays(mr_off, case["params"][1], case["params"][2], device=dev)
+    st.forward(P_off, t(case["rot"][:1]), t(case["shift"][:1]), t(case["ctf"][:1]), t(case["obs"][:1]))
+    s = st.stats(check=False)
+    assert s["entries"] == 0 and s["overflow"] == 1 and s["status"] == b.GEM_E_CAPACITY
+    s = st.stats(check=False)
+    assert s["overflow"] == 0 and s["status"] == b.GEM_OK
 
 
 def test_workspace_has_no_cubic_term(gem):
