@@ -345,6 +345,46 @@ def test_host_pipeline_matches_device_steps(gem):
     assert np.isfinite(lh.numpy()).all() and lh[-1] > 0
 
 
+@pytest.mark.parametrize("D", [64, 48])
+def test_forward_without_outputs(gem, orc, D):
+    """The training/bench path: no projection or prediction requested, so the render writes the
+    workspace's projection buffer, which the column kernel then reuses for the packed gradient
+    rows (row path, D = 64) or the C2R output (2D path, D = 48).  Loss and gradients equal those
+    of the run that returns the images (bitwise on the row path; the 2D cuFFT plans may pick
+    another kernel for another input alignment, so there to rounding) and the oracle's."""
+    case = make_case("T", B=3, seed=33, N=900, D=D)
+    w = case["w"]
+    st = gem.GemStep(gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=3, list_capacity=1 << 18))
+    dev = st.device
+    P = gem.SoA.from_arrays(*case["params"], device=dev)
+    t = lambda a: torch.from_numpy(a).to(dev)
+    args = [t(case[k]) for k in ("rot", "shift", "ctf", "obs")]
+    loss_a = st.forward(P, *args).cpu().numpy().copy()
+    grad_a = gem.SoA.zeros(w.N, dev)
+    st.backward(P, grad_a)
+    proj = torch.empty(3, w.D, w.D, device=dev)
+    pred = torch.empty(3, w.D, w.D, device=dev)
+    loss_b = st.forward(P, *args, proj=proj, pred=pred).cpu().numpy().copy()
+    grad_b = gem.SoA.zeros(w.N, dev)
+    st.backward(P, grad_b)
+    torch.cuda.synchronize()
+    assert st.stats(check=False)["status"] == 0
+    if D == 64:
+        assert np.array_equal(loss_a, loss_b)
+        assert torch.equal(grad_a.t, grad_b.t)
+    else:
+        assert np.allclose(loss_a, loss_b, rtol=1e-6, atol=0)
+        gb = grad_b.t.permute(1, 0, 2).reshape(w.N, 12).cpu().numpy()
+        g_a = grad_a.t.permute(1, 0, 2).reshape(w.N, 12).cpu().numpy()
+        for name, cols in CLASSES.items():
+            assert maxnorm_rel(g_a[:, cols], gb[:, cols]) < 1e-5, name
+    o = oracle_out(orc, case, want=())
+    assert np.all(np.abs(loss_a[:-1] - o["loss"]) < LOSS_TOL * o["loss"])
+    ga = grad_a.t.permute(1, 0, 2).reshape(w.N, 12).cpu().numpy()
+    for name, cols in CLASSES.items():
+        assert maxnorm_rel(ga[:, cols], o["grad"][:, cols]) < GRAD_TOL, name
+
+
 def test_R_config_full_size(gem, orc):
     """BASELINE config R at full size (N = 50,000, D = 256, px = 1.31 A) in the bench's launch
     configuration (default 8x8 tiles, non-fused), one particle: bit-exact lists and the whole
