@@ -198,6 +198,11 @@ def run_reference(args, rank, world):
     bounded sample per step (rank 0 only)."""
     if rank != 0:
         return 0
+    if world > 1:
+        # torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 is the only rank that works here, so
+        # it takes the host's cores (read by libgomp when the oracle library is first loaded)
+        os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+                                            else os.cpu_count())
     w = synth.CONFIGS[args.config]
     t1 = oracle_step_sample(w, 1)
     budget = 150.0
