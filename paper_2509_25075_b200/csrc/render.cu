@@ -437,7 +437,8 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
 // image-space gradient (q0 = L_amp amp, l_mx, l_my, G_hat 00/01/11, in Angstrom units).  That is
 // transformed to the world frame with W_i = P_i^T and summed over the chunk in particle order:
 //   G_mu += W^T (l_mx, l_my, 0),  G_Sigma += W^T [G_hat 0; 0 0] W,  L_rho += q0 / rho,
-// and the chunk's ten sums go to slot (chunk, j) (coalesced, one writer); k_bwd_reduce adds the
+// (the ten running sums live in shared memory, which keeps the two-row-pair walk below within 64
+// registers), and the chunk's ten sums go to slot (chunk, j) (coalesced, one writer); k_bwd_reduce adds the
 // chunks in a fixed order: deterministic, no atomics, 10 floats per (chunk, j) of traffic
 // instead of 6 per (i, j).
 constexpr int kBwdBlock = 256, kBwdP = 8;   // threads per block, particles per thread
@@ -456,7 +457,10 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
   }
   __syncthreads();
   if (j >= c.N) return;
-  float vacc[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  __shared__ float sacc[10][kBwdBlock];   // the chunk's ten running sums (off the registers)
+  float *vacc = &sacc[0][threadIdx.x];     // vacc[k * kBwdBlock] = sum k
+#pragma unroll
+  for (int k = 0; k < 10; ++k) vacc[k * kBwdBlock] = 0.f;
 #pragma unroll 1
   for (int p = 0; p < np; ++p) {
   const int i = i0 + p;
@@ -495,54 +499,72 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
   }
   const float wf = (float)wd;
   const float2 S2 = make_float2(S, S);
+  auto fold = [&](float2 C, float2 Q, float2 Z, float dyA, float dyB) {
+    M0 += C.x + C.y;
+    MQ += Q.x + Q.y;
+    MZ += Z.x + Z.y;
+    Y0 = fmaf(dyA, C.x, fmaf(dyB, C.y, Y0));
+    YQ = fmaf(dyA, Q.x, fmaf(dyB, Q.y, YQ));
+    YY = fmaf(dyA * dyA, C.x, fmaf(dyB * dyB, C.y, YY));
+  };
   // row pairs at absolute (2m, 2m + 1); r = row of the pair's first row relative to vlo (-1 when
   // vlo is odd: that row is outside the box and carries E = 0)
+  const float2 *g0 = reinterpret_cast<const float2 *>(gi);
+  if (!slow) {
+    // two row pairs per iteration (independent chains: twice the loads in flight); rows outside
+    // the box carry E = 0, and a pair wholly below the box re-reads the first pair's memory
+    auto adv = [&]() { El *= V; V *= W; Rl *= Kb; };
 #pragma unroll 1
-  for (int r = -(vlo & 1); r < ht; r += 2) {
-    const bool vA = r >= 0, vB = r + 1 < ht;
-    const float dyA = dy0 + (float)r, dyB = dyA + 1.f;
-    const float2 *gp = reinterpret_cast<const float2 *>(gi) + (size_t)((r + (vlo & 1)) >> 1) * c.D;
-    float2 C = make_float2(0.f, 0.f), Q = C, Z = C;
-    if (!slow) {
-      float2 E2, R2;
-      E2.x = vA ? El : 0.f;
-      R2.x = vA ? Rl : 0.f;
-      if (vA) { El *= V; V *= W; Rl *= Kb; }
-      E2.y = vB ? El : 0.f;
-      R2.y = vB ? Rl : 0.f;
-      if (vB) { El *= V; V *= W; Rl *= Kb; }
+    for (int r = -(vlo & 1); r < ht; r += 4) {
+      const bool a0 = r >= 0, b0 = r + 1 < ht, a1 = r + 2 < ht, b1 = r + 3 < ht;
+      const float2 *gp0 = g0 + (size_t)((r + (vlo & 1)) >> 1) * c.D;
+      const float2 *gp1 = a1 ? gp0 + c.D : gp0;
+      float2 E0, R0, E1, R1;
+      E0.x = a0 ? El : 0.f; R0.x = a0 ? Rl : 0.f; if (a0) adv();
+      E0.y = b0 ? El : 0.f; R0.y = b0 ? Rl : 0.f; if (b0) adv();
+      E1.x = a1 ? El : 0.f; R1.x = a1 ? Rl : 0.f; if (a1) adv();
+      E1.y = b1 ? El : 0.f; R1.y = b1 ? Rl : 0.f; if (b1) adv();
+      float2 C0 = make_float2(0.f, 0.f), Q0 = C0, Z0 = C0, C1 = C0, Q1 = C0, Z1 = C0;
+      auto step = [&](float2 ga, float2 gb) {
+        const float2 Ea = MK ? make_float2(E0.x >= ethr ? E0.x : 0.f, E0.y >= ethr ? E0.y : 0.f) : E0;
+        const float2 Eb = MK ? make_float2(E1.x >= ethr ? E1.x : 0.f, E1.y >= ethr ? E1.y : 0.f) : E1;
+        C0 = __ffma2_rn(ga, Ea, C0);   // C += h, h = g e
+        C1 = __ffma2_rn(gb, Eb, C1);
+        Q0 = __fadd2_rn(Q0, C0);
+        Q1 = __fadd2_rn(Q1, C1);
+        Z0 = __fadd2_rn(Z0, Q0);
+        Z1 = __fadd2_rn(Z1, Q1);
+        E0 = __fmul2_rn(E0, R0);
+        E1 = __fmul2_rn(E1, R1);
+        R0 = __fmul2_rn(R0, S2);
+        R1 = __fmul2_rn(R1, S2);
+      };
       // column pairs at even absolute columns are read with one 128-bit load (two columns of the
       // row pair); an odd first column and an odd last column are peeled
       int k = 0;
-      auto step = [&](float2 g2) {
-        const float2 Em = MK ? make_float2(E2.x >= ethr ? E2.x : 0.f, E2.y >= ethr ? E2.y : 0.f) : E2;
-        C = __ffma2_rn(g2, Em, C);   // C += h, h = g e
-        Q = __fadd2_rn(Q, C);
-        Z = __fadd2_rn(Z, Q);
-        E2 = __fmul2_rn(E2, R2);
-        R2 = __fmul2_rn(R2, S2);
-      };
       if (ulo & 1) {
-        step(__ldg(gp));
+        step(__ldg(gp0), __ldg(gp1));
         k = 1;
       }
 #pragma unroll 1
-      for (; k + 3 < wd; k += 4) {   // two 128-bit loads in flight
-        const float4 g4 = __ldg(reinterpret_cast<const float4 *>(gp + k));
-        const float4 h4 = __ldg(reinterpret_cast<const float4 *>(gp + k + 2));
-        step(make_float2(g4.x, g4.y));
-        step(make_float2(g4.z, g4.w));
-        step(make_float2(h4.x, h4.y));
-        step(make_float2(h4.z, h4.w));
+      for (; k + 1 < wd; k += 2) {
+        const float4 ga = __ldg(reinterpret_cast<const float4 *>(gp0 + k));
+        const float4 gb = __ldg(reinterpret_cast<const float4 *>(gp1 + k));
+        step(make_float2(ga.x, ga.y), make_float2(gb.x, gb.y));
+        step(make_float2(ga.z, ga.w), make_float2(gb.z, gb.w));
       }
-      if (k + 1 < wd) {
-        const float4 g4 = __ldg(reinterpret_cast<const float4 *>(gp + k));
-        step(make_float2(g4.x, g4.y));
-        step(make_float2(g4.z, g4.w));
-        k += 2;
-      }
-      if (k < wd) step(__ldg(gp + k));
-    } else {   // direct evaluation, exp per pixel; sums converted to (C, Q, Z) form
+      if (k < wd) step(__ldg(gp0 + k), __ldg(gp1 + k));
+      const float dyA = dy0 + (float)r;
+      fold(C0, Q0, Z0, dyA, dyA + 1.f);
+      fold(C1, Q1, Z1, dyA + 2.f, dyA + 3.f);
+    }
+  } else {
+#pragma unroll 1
+    for (int r = -(vlo & 1); r < ht; r += 2) {   // direct evaluation, exp per pixel, (C, Q, Z) form
+      const bool vA = r >= 0, vB = r + 1 < ht;
+      const float dyA = dy0 + (float)r, dyB = dyA + 1.f;
+      const float2 *gp = g0 + (size_t)((r + (vlo & 1)) >> 1) * c.D;
+      float2 C = make_float2(0.f, 0.f), Q = C, Z = C;
       const float fA = fmaf(dyA, fmaf(nc, dyA, Gx), Fx), fB = fmaf(dyB, fmaf(nc, dyB, Gx), Fx);
       const float gA = fmaf(nb2, dyA, D0), gB = fmaf(nb2, dyB, D0);
 #pragma unroll 1
@@ -558,13 +580,8 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
         Q.x = fmaf(hA, tf, Q.x); Q.y = fmaf(hB, tf, Q.y);
         Z.x = fmaf(hA, zt, Z.x); Z.y = fmaf(hB, zt, Z.y);
       }
+      fold(C, Q, Z, dyA, dyB);
     }
-    M0 += C.x + C.y;
-    MQ += Q.x + Q.y;
-    MZ += Z.x + Z.y;
-    Y0 = fmaf(dyA, C.x, fmaf(dyB, C.y, Y0));
-    YQ = fmaf(dyA, Q.x, fmaf(dyB, Q.y, YQ));
-    YY = fmaf(dyA * dyA, C.x, fmaf(dyB * dyB, C.y, YY));
   }
   // (C, Q, Z) moments -> dx-moments: dx = dx0 + k = dxw - t with dxw = dx0 + wd
   const float dxw = dx0 + wf, Mt2 = fmaf(2.f, MZ, -MQ);   // Mt2 = sum h t^2
@@ -585,23 +602,23 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
   // world frame, summed over the chunk in particle order
   const float W0[3] = {sW[p][0], sW[p][1], sW[p][2]}, W1[3] = {sW[p][3], sW[p][4], sW[p][5]};
   const float lmx = Lmx * inv_px, lmy = Lmy * inv_px;
-  vacc[0] += La * amp;
-  vacc[1] += lmx * W0[0] + lmy * W1[0];
-  vacc[2] += lmx * W0[1] + lmy * W1[1];
-  vacc[3] += lmx * W0[2] + lmy * W1[2];
+  vacc[0 * kBwdBlock] += La * amp;
+  vacc[1 * kBwdBlock] += lmx * W0[0] + lmy * W1[0];
+  vacc[2 * kBwdBlock] += lmx * W0[1] + lmy * W1[1];
+  vacc[3 * kBwdBlock] += lmx * W0[2] + lmy * W1[2];
   float t0[3], t1[3];
 #pragma unroll
   for (int l = 0; l < 3; ++l) { t0[l] = G00 * W0[l] + G01 * W1[l]; t1[l] = G01 * W0[l] + G11 * W1[l]; }
-  vacc[4] += W0[0] * t0[0] + W1[0] * t1[0];
-  vacc[5] += W0[0] * t0[1] + W1[0] * t1[1];
-  vacc[6] += W0[0] * t0[2] + W1[0] * t1[2];
-  vacc[7] += W0[1] * t0[1] + W1[1] * t1[1];
-  vacc[8] += W0[1] * t0[2] + W1[1] * t1[2];
-  vacc[9] += W0[2] * t0[2] + W1[2] * t1[2];
+  vacc[4 * kBwdBlock] += W0[0] * t0[0] + W1[0] * t1[0];
+  vacc[5 * kBwdBlock] += W0[0] * t0[1] + W1[0] * t1[1];
+  vacc[6 * kBwdBlock] += W0[0] * t0[2] + W1[0] * t1[2];
+  vacc[7 * kBwdBlock] += W0[1] * t0[1] + W1[1] * t1[1];
+  vacc[8 * kBwdBlock] += W0[1] * t0[2] + W1[1] * t1[2];
+  vacc[9 * kBwdBlock] += W0[2] * t0[2] + W1[2] * t1[2];
   }
   float *dst = slots + (size_t)chunk * 10 * c.N + j;
 #pragma unroll
-  for (int k = 0; k < 10; ++k) dst[(size_t)k * c.N] = vacc[k];
+  for (int k = 0; k < 10; ++k) dst[(size_t)k * c.N] = vacc[k * kBwdBlock];
 }
 
 // dL/dI (B images of D x D, row-major, from the C2R) -> row-pair interleaved layout read by
