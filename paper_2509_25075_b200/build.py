@@ -24,7 +24,7 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-    "-Xptxas", "-v",
+    "-Xptxas", "-v", "-Xptxas", "-warn-spills",
     "-shared", "-cudart", "shared",
     "-I" + os.path.join(ROOT, "include"),
 ]
@@ -57,7 +57,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libgem.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as f:
+    # resource report (registers, spills) for the kernels; untracked, under build/
+    os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+    with open(os.path.join(ROOT, "build", "ptxas.log"), "w") as f:
         f.write(res.stderr)
     os.replace(tmp, LIB)
     return LIB
