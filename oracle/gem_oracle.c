@@ -143,11 +143,17 @@ typedef struct {
   int ok;
 } orc_gauss_t;
 
-static orc_gauss_t *prep_all(int N, const double *quat, const double *log_scale) {
+/* O1 for all Gaussians.  Reading L18: a Gaussian is degenerate (skipped in every pair, zero
+ * gradient row, counted) if |q| = 0 or anything it is made of is non-finite: q, Sigma, |Sigma|
+ * (orc_gauss) and also its centre mu and density rho, which reach every pair through m and amp. */
+static orc_gauss_t *prep_all(int N, const double *mean_rho, const double *quat, const double *log_scale) {
   orc_gauss_t *g = (orc_gauss_t *)calloc((size_t)N, sizeof(orc_gauss_t));
-  for (int j = 0; j < N; ++j)
+  for (int j = 0; j < N; ++j) {
     g[j].ok = orc_gauss(quat + 4 * j, log_scale + 4 * j, g[j].R, g[j].Sig, &g[j].detS, &g[j].qn,
                         g[j].qhat);
+    const double *m = mean_rho + 4 * j;
+    if (!(isfinite(m[0]) && isfinite(m[1]) && isfinite(m[2]) && isfinite(m[3]))) g[j].ok = 0;
+  }
   return g;
 }
 
@@ -156,7 +162,7 @@ static orc_gauss_t *prep_all(int N, const double *quat, const double *log_scale)
 void orc_splats(int N, int B, const double *mean_rho, const double *log_scale, const double *quat,
                 const double *rot, const double *shift, int D, double px, double k, double tau,
                 int32_t *aabb, int32_t *visible, double *splat) {
-  orc_gauss_t *g = prep_all(N, quat, log_scale);
+  orc_gauss_t *g = prep_all(N, mean_rho, quat, log_scale);
 #pragma omp parallel for collapse(2) schedule(static)
   for (int i = 0; i < B; ++i)
     for (int j = 0; j < N; ++j) {
@@ -220,7 +226,7 @@ static int pix_keep(const orc_splat_t *s, double Q, int pixmask, double k, doubl
 long long orc_lists_pixmask(int N, int B, const double *mean_rho, const double *log_scale, const double *quat,
                             const double *rot, const double *shift, int D, double px, double k, double tau, int T,
                             int pixmask, int32_t *tile_off, int64_t *ids_base, int32_t *ids, long long cap) {
-  orc_gauss_t *g = prep_all(N, quat, log_scale);
+  orc_gauss_t *g = prep_all(N, mean_rho, quat, log_scale);
   orc_splat_t *sp = (orc_splat_t *)malloc((size_t)B * N * sizeof(orc_splat_t));
   for (int i = 0; i < B; ++i)
     for (int j = 0; j < N; ++j)
@@ -279,7 +285,7 @@ static int pix_keep(const orc_splat_t *s, double Q, int pixmask, double k, doubl
 void orc_project(int N, int B, const double *mean_rho, const double *log_scale, const double *quat,
                  const double *rot, const double *shift, int D, double px, double k, double tau,
                  int masked, double *img) {
-  orc_gauss_t *g = prep_all(N, quat, log_scale);
+  orc_gauss_t *g = prep_all(N, mean_rho, quat, log_scale);
   orc_splat_t *sp = (orc_splat_t *)malloc((size_t)B * N * sizeof(orc_splat_t));
 #pragma omp parallel for collapse(2) schedule(static)
   for (int i = 0; i < B; ++i)
@@ -315,7 +321,7 @@ void orc_project(int N, int B, const double *mean_rho, const double *log_scale, 
 void orc_project_pixels(int N, const double *mean_rho, const double *log_scale, const double *quat,
                         const double *rot, const double *shift, int D, double px, double k, double tau,
                         int masked, int npix, const int32_t *pix, double *out) {
-  orc_gauss_t *g = prep_all(N, quat, log_scale);
+  orc_gauss_t *g = prep_all(N, mean_rho, quat, log_scale);
   orc_splat_t *sp = (orc_splat_t *)malloc((size_t)N * sizeof(orc_splat_t));
 #pragma omp parallel for schedule(static)
   for (int j = 0; j < N; ++j)
@@ -462,7 +468,7 @@ double orc_loss_grad(int N, int B, const double *mean_rho, const double *log_sca
                      const int32_t *frozen_vis, double *loss, double *proj_out, double *pred_out,
                      double *gimg_out, double *grad, double *acc_out) {
   size_t DD = (size_t)D * D;
-  orc_gauss_t *g = prep_all(N, quat, log_scale);
+  orc_gauss_t *g = prep_all(N, mean_rho, quat, log_scale);
   orc_splat_t *sp = (orc_splat_t *)malloc((size_t)B * N * sizeof(orc_splat_t));
 #pragma omp parallel for collapse(2) schedule(static)
   for (int i = 0; i < B; ++i)
@@ -658,7 +664,7 @@ void orc_adam(int N, double *params, const double *grad, double *m, double *v, l
  * vol [Dv][Dv][Dv] with x fastest: vol[(c*Dv + b)*Dv + a]. */
 void orc_volume(int N, const double *mean_rho, const double *log_scale, const double *quat, int Dv,
                 double vs, double k, int masked, double *vol) {
-  orc_gauss_t *g = prep_all(N, quat, log_scale);
+  orc_gauss_t *g = prep_all(N, mean_rho, quat, log_scale);
   double *inv = (double *)malloc(sizeof(double) * 9 * (size_t)N);
   int *box = (int *)malloc(sizeof(int) * 6 * (size_t)N);
   double half = (double)(Dv / 2);

@@ -422,7 +422,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
   float4 *acc = at<float4>(ctx, L.acc);
   double *lpart = at<double>(ctx, L.loss_part);
   if (ctx->fused) CK(cudaMemsetAsync(acc, 0, sizeof(float4) * 3 * (size_t)c.N, s));
-  { Prof p(ctx, s, P_PREP); launch_prep(c, (const float4 *)params->log_scale, (const float4 *)params->quat, prep, st, s, ctx->launches); }
+  { Prof p(ctx, s, P_PREP); launch_prep(c, (const float4 *)params->mean_rho, (const float4 *)params->log_scale, (const float4 *)params->quat, prep, st, s, ctx->launches); }
   const size_t DD = D * D;
   int p0 = 0, nb = 0;
   for (p0 = 0; p0 < B; p0 += ctx->W) {   // one wave (all of B when not fused)
@@ -533,13 +533,13 @@ gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_
                         at<float>(ctx, L.slots), s, ctx->launches);
     }
     Prof p(ctx, s, P_BWD_REDUCE);
-    launch_reduce_finalize(c, ctx->last_B, at<float>(ctx, L.slots), (const float4 *)params->mean_rho,
+    launch_reduce_finalize(c, ctx->last_B, at<float>(ctx, L.slots), at<GaussPrep>(ctx, L.prep), (const float4 *)params->mean_rho,
                            (const float4 *)params->log_scale, (const float4 *)params->quat, (float4 *)grad->mean_rho,
                            (float4 *)grad->log_scale, (float4 *)grad->quat, at<DevStats>(ctx, L.stats), s,
                            ctx->launches);
   } else {   // fused mode: the forward already reduced every wave into acc
     Prof pf(ctx, s, P_FINALIZE);
-    launch_finalize(c, acc, (const float4 *)params->mean_rho, (const float4 *)params->log_scale,
+    launch_finalize(c, acc, at<GaussPrep>(ctx, L.prep), (const float4 *)params->mean_rho, (const float4 *)params->log_scale,
                     (const float4 *)params->quat, (float4 *)grad->mean_rho, (float4 *)grad->log_scale,
                     (float4 *)grad->quat, at<DevStats>(ctx, L.stats), s, ctx->launches);
   }

@@ -157,8 +157,8 @@ __device__ __forceinline__ unsigned ord32(float z) {
 
 // ---------------------------------------------------------------- kernels
 namespace gem {
-void launch_prep(const CfgDev &c, const float4 *log_scale, const float4 *quat, GaussPrep *prep, DevStats *st,
-                 cudaStream_t s, int &launches);
+void launch_prep(const CfgDev &c, const float4 *mean_rho, const float4 *log_scale, const float4 *quat, GaussPrep *prep,
+                 DevStats *st, cudaStream_t s, int &launches);
 void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
                         const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, DevStats *st,
                         cudaStream_t s, int &launches);
@@ -189,10 +189,10 @@ void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float 
                        cudaStream_t s, int &launches);
 void launch_bwd_reduce(const CfgDev &c, int B, const float *slots, const float4 *mean_rho, float4 *acc, cudaStream_t s,
                        int &launches);
-void launch_reduce_finalize(const CfgDev &c, int B, const float *slots, const float4 *mean_rho, const float4 *log_scale,
-                            const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
+void launch_reduce_finalize(const CfgDev &c, int B, const float *slots, const GaussPrep *prep, const float4 *mean_rho,
+                            const float4 *log_scale, const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
                             int &launches);
-void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho, const float4 *log_scale,
+void launch_finalize(const CfgDev &c, const float4 *acc, const GaussPrep *prep, const float4 *mean_rho, const float4 *log_scale,
                      const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
                      int &launches);
 void launch_adam(int N, float4 *p_mr, float4 *p_ls, float4 *p_q, const float4 *g_mr, const float4 *g_ls,

@@ -12,14 +12,16 @@
 namespace gem {
 namespace {
 
+// Degenerate Gaussians (the fp64 prep's flag, k_prep: the predicate of oracle O1, reading L18)
+// get an exactly-zero gradient row.
 __device__ __forceinline__ void finalize_j(int j, int no_rot, float4 a0, float4 a1, float4 a2,
-                                           const float4 *__restrict__ mr, const float4 *__restrict__ ls,
+                                           const GaussPrep *__restrict__ prep, const float4 *__restrict__ mr, const float4 *__restrict__ ls,
                                            const float4 *__restrict__ q, float4 *__restrict__ g_mr,
                                            float4 *__restrict__ g_ls, float4 *__restrict__ g_q, DevStats *st) {
   const float4 qq = q[j], ss = ls[j];
   const float rho = mr[j].w;
   const float n = sqrtf(qq.x * qq.x + qq.y * qq.y + qq.z * qq.z + qq.w * qq.w);
-  if (!(n > 0.f) || !isfinite(n)) {
+  if (prep[j].ok == 0.0 || !(n > 0.f)) {
     g_mr[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     g_ls[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     g_q[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -67,18 +69,19 @@ __device__ __forceinline__ void finalize_j(int j, int no_rot, float4 a0, float4 
 }
 
 __global__ void __launch_bounds__(256) k_finalize(int N, int no_rot, const float4 *__restrict__ acc,
-                                                  const float4 *__restrict__ mr, const float4 *__restrict__ ls,
+                                                  const GaussPrep *__restrict__ prep, const float4 *__restrict__ mr, const float4 *__restrict__ ls,
                                                   const float4 *__restrict__ q, float4 *__restrict__ g_mr,
                                                   float4 *__restrict__ g_ls, float4 *__restrict__ g_q, DevStats *st) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
-  finalize_j(j, no_rot, acc[3 * (size_t)j], acc[3 * (size_t)j + 1], acc[3 * (size_t)j + 2], mr, ls, q, g_mr, g_ls,
+  finalize_j(j, no_rot, acc[3 * (size_t)j], acc[3 * (size_t)j + 1], acc[3 * (size_t)j + 2], prep, mr, ls, q, g_mr, g_ls,
              g_q, st);
 }
 
 // One batch (not fused): the backward's chunk sums [chunk][10][N] (render.cu k_render_bwd) are
 // added in chunk order and finalized in the same thread (no accumulator round trip).
 __global__ void __launch_bounds__(256) k_reduce_finalize(int nchunk, int N, int no_rot, const float *__restrict__ slots,
+                                                         const GaussPrep *__restrict__ prep,
                                                          const float4 *__restrict__ mr, const float4 *__restrict__ ls,
                                                          const float4 *__restrict__ q, float4 *__restrict__ g_mr,
                                                          float4 *__restrict__ g_ls, float4 *__restrict__ g_q,
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(256) k_reduce_finalize(int nchunk, int N, int 
   }
   const float rho = mr[j].w;
   finalize_j(j, no_rot, make_float4(rho != 0.f ? v[0] / rho : 0.f, v[1], v[2], v[3]), make_float4(v[4], v[5], v[6], v[7]),
-             make_float4(v[8], v[9], 0.f, 0.f), mr, ls, q, g_mr, g_ls, g_q, st);
+             make_float4(v[8], v[9], 0.f, 0.f), prep, mr, ls, q, g_mr, g_ls, g_q, st);
 }
 
 __device__ __forceinline__ float adam1(float p, float g, float &m, float &v, float lr, float b1, float b2, float eps,
@@ -148,18 +151,18 @@ __global__ void __launch_bounds__(256) k_adam(int N, AdamArgs A) {
 
 }  // namespace
 
-void launch_reduce_finalize(const CfgDev &c, int B, const float *slots, const float4 *mean_rho, const float4 *log_scale,
-                            const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
+void launch_reduce_finalize(const CfgDev &c, int B, const float *slots, const GaussPrep *prep, const float4 *mean_rho,
+                            const float4 *log_scale, const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
                             int &launches) {
   k_reduce_finalize<<<(c.N + 255) / 256, 256, 0, s>>>(bwd_chunks(B), c.N, c.flags & GEM_FLAG_NO_ROTATION ? 1 : 0, slots,
-                                                      mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
+                                                      prep, mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
   ++launches;
 }
 
-void launch_finalize(const CfgDev &c, const float4 *acc, const float4 *mean_rho, const float4 *log_scale,
+void launch_finalize(const CfgDev &c, const float4 *acc, const GaussPrep *prep, const float4 *mean_rho, const float4 *log_scale,
                      const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
                      int &launches) {
-  k_finalize<<<(c.N + 255) / 256, 256, 0, s>>>(c.N, c.flags & GEM_FLAG_NO_ROTATION ? 1 : 0, acc, mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
+  k_finalize<<<(c.N + 255) / 256, 256, 0, s>>>(c.N, c.flags & GEM_FLAG_NO_ROTATION ? 1 : 0, acc, prep, mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
   ++launches;
 }
 

@@ -27,12 +27,15 @@ __device__ __forceinline__ double dv(double a, double b) { return __ddiv_rn(a, b
 
 // ----------------------------------------------------------------- a1 prep
 // q_hat = q/|q|, R(q_hat), sigma^2 = exp(2 s), Sigma = R diag(sigma^2) R^T,
-// |Sigma| = exp(2 (s0+s1+s2))   (Eq. 4).
-__global__ void __launch_bounds__(256) k_prep(int N, const float4 *__restrict__ ls, const float4 *__restrict__ q,
-                                              GaussPrep *__restrict__ prep, DevStats *st) {
+// |Sigma| = exp(2 (s0+s1+s2))   (Eq. 4).  Degenerate (reading L18: skipped
+// in every pair, zero gradient row, counted): |q| = 0, or q, Sigma, |Sigma|, mu or rho non-finite.
+__global__ void __launch_bounds__(256) k_prep(int N, const float4 *__restrict__ mr, const float4 *__restrict__ ls,
+                                              const float4 *__restrict__ q, GaussPrep *__restrict__ prep,
+                                              DevStats *st) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
   float4 qq = q[j], ss = ls[j];
+  const float4 m4 = mr[j];
   double w = qq.x, x = qq.y, y = qq.z, z = qq.w;
   double n = sqrt(da(da(da(dm(w, w), dm(x, x)), dm(y, y)), dm(z, z)));
   GaussPrep p;
@@ -60,7 +63,8 @@ __global__ void __launch_bounds__(256) k_prep(int N, const float4 *__restrict__ 
     }
     p.detS = exp(dm(2.0, da(da(s0, s1), s2)));
     p.sdetS = exp(da(da(s0, s1), s2));   // |Sigma|^{1/2} (amplitude only, not bound-critical)
-    ok = isfinite(p.detS) && isfinite(p.sig[0]) && isfinite(p.sig[3]) && isfinite(p.sig[5]);
+    ok = isfinite(p.detS) && isfinite(p.sig[0]) && isfinite(p.sig[3]) && isfinite(p.sig[5]) && isfinite(m4.x) &&
+         isfinite(m4.y) && isfinite(m4.z) && isfinite(m4.w);
   }
   if (!ok) {
 #pragma unroll
@@ -446,13 +450,11 @@ __global__ void __launch_bounds__(k1pThreads) k_scan_1p(const int *__restrict__ 
 
 // --------------------------------------------------------------- a3 fill
 // One CTA of 4 warps per (particle, chunk of kChunk Gaussians); warp w owns the sub-chunk w.
-// Pass 1 counts each sub-chunk's entries per tile (smem integer atomics, order-free); a per-tile
-// scan over the 4 sub-chunks, seeded with the chunk's global offset, gives each warp its
-// cursors; pass 2 visits the warp's Gaussians 32 per step and, for each tile slot (dv, du) of
-// their tile rectangles in turn, ranks the step's entries per tile with __match_any_sync.  The
-// order within a tile's list is therefore (chunk, sub-chunk, step, slot, Gaussian id): a
-// deterministic function of the boxes (so the forward stays bitwise reproducible), and the
-// per-tile sets equal the oracle's (reading L9: only the set and its determinism matter).
+// The splat kernel counted each sub-chunk's entries per tile; those counts, seeded with the
+// chunk's global offset (the device scan), give each warp its per-tile cursors; the warp then
+// visits its Gaussians 32 per step (consecutive ids) and emits each step's entries per tile in
+// lane order.  Chunks, sub-chunks and steps are in id order, so every tile's list is in
+// ascending Gaussian id: the oracle's O4 list, element by element.
 
 
 // ZK (GEM_FLAG_ZSORT): entries are written as (id, z-sort key ord32(fp32(z_ij))) pairs to
@@ -467,7 +469,9 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
                                                           const float *__restrict__ rot, uint2 *__restrict__ zpair,
                                                           const SplatRec *__restrict__ rec) {
   extern __shared__ int cnt[];   // [kFillWarps][NT] cursors
+  __shared__ unsigned smask[kFillWarps * 64];   // per warp: lane sets of the step's tiles
   const int i = blockIdx.y, ch = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < kFillWarps * 64; t += blockDim.x) smask[t] = 0u;
   int *mine = cnt + w * c.NT;
   const int jsub = ch * kChunk + w * kSub;
   const uint2 *boxi = box + (size_t)i * c.N;
@@ -512,28 +516,112 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
       ucen = (float)ulo + r.f0.x; vcen = (float)vlo + r.f0.y;
       ca = r.f0.z; cb = r.f0.w; cc = r.f1.x; tq = keep_q(c, r.f1.y);
     }
-    // slot-major order: every lane's tile (dv, du) of its rectangle, (dv, du) ascending, then lane
-    const int mu = __reduce_max_sync(0xffffffffu, (unsigned)max(ntu, 0));
-    const int mv = __reduce_max_sync(0xffffffffu, (unsigned)ntv);
-    for (int dv = 0; dv < mv; ++dv) {
-      for (int du = 0; du < mu; ++du) {
-        const int tu = tu0 + du, tv = tv0 + dv;
-        const bool active = du < ntu && dv < ntv &&
-                            (!pixmask || tile_kept(ucen, vcen, ca, cb, cc, tq, max(ulo, tu << c.tshift),
-                                                   min(uhi, (tu << c.tshift) + c.T - 1), max(vlo, tv << c.tshift),
-                                                   min(vhi, (tv << c.tshift) + c.T - 1)));
-        const int t = tv * c.nt + tu;
-        const unsigned m = __match_any_sync(0xffffffffu, active ? t : -1);
-        const int rank = __popc(m & lt);
-        if (active) {
-          const int slot = mine[t] + rank;
-          if ((int64_t)slot < c.cap) {
-            if (ZK) zpair[slot] = make_uint2((unsigned)j, key);
-            else ids[slot] = j;
+    // Ascending Gaussian id within each tile (O4 order, reading L9): the step's 32 Gaussians are
+    // consecutive ids, so a tile's entries from this step go in lane order.  Each lane keeps a
+    // bit mask of the cells of its tile rectangle still to be emitted; per round the first lane
+    // with work names its first pending tile, a ballot of the lanes whose rectangle holds that
+    // tile gives each its rank, and the tile's cursor advances once (rounds = distinct tiles the
+    // step touches).  Rectangles wider than 8 or taller than 4 tiles (huge boxes) send the step to a serial
+    // path: lanes one after the other, the warp spreading each rectangle over its 32 lanes.
+    const bool act = ntu > 0;
+    auto kept = [&](int tu, int tv) {
+      return !pixmask || tile_kept(ucen, vcen, ca, cb, cc, tq, max(ulo, tu << c.tshift),
+                                   min(uhi, (tu << c.tshift) + c.T - 1), max(vlo, tv << c.tshift),
+                                   min(vhi, (tv << c.tshift) + c.T - 1));
+    };
+    auto put = [&](int slot, int jj, unsigned kk) {
+      if ((int64_t)slot < c.cap) {
+        if (ZK) zpair[slot] = make_uint2((unsigned)jj, kk);
+        else ids[slot] = jj;
+      }
+    };
+    // Usual case: the union of the step's rectangles spans <= 64 tiles.  Each lane ORs its lane
+    // bit into a per-warp shared word per tile of its rectangle; a tile's word is then the set
+    // of the step's lanes holding it: rank = lanes below, and the lowest lane advances the
+    // cursor and clears the word.
+    const int ux0 = __reduce_min_sync(0xffffffffu, act ? tu0 : 0x7fffffff);
+    if (ux0 == 0x7fffffff) continue;   // no visible Gaussian in this step
+    const int vy0 = __reduce_min_sync(0xffffffffu, act ? tv0 : 0x7fffffff);
+    const int uw = (int)__reduce_max_sync(0xffffffffu, act ? (unsigned)(tu0 + ntu) : 0u) - ux0;
+    const int uh = (int)__reduce_max_sync(0xffffffffu, act ? (unsigned)(tv0 + ntv) : 0u) - vy0;
+    if (uw * uh <= 64) {
+      unsigned *sm = smask + 64 * w;
+      const int cbase = (tv0 - vy0) * uw + (tu0 - ux0);
+      if (act)
+        for (int dv = 0; dv < ntv; ++dv)
+          for (int du = 0; du < ntu; ++du)
+            if (kept(tu0 + du, tv0 + dv)) atomicOr(&sm[cbase + dv * uw + du], 1u << lane);
+      __syncwarp();
+      if (act)
+        for (int dv = 0; dv < ntv; ++dv)
+          for (int du = 0; du < ntu; ++du) {
+            const unsigned m = sm[cbase + dv * uw + du];
+            if ((m >> lane) & 1u) put(mine[(tv0 + dv) * c.nt + tu0 + du] + __popc(m & lt), j, key);
           }
+      __syncwarp();
+      if (act)
+        for (int dv = 0; dv < ntv; ++dv)
+          for (int du = 0; du < ntu; ++du) {
+            const int cc_ = cbase + dv * uw + du;
+            const unsigned m = sm[cc_];
+            if (((m >> lane) & 1u) && !(m & lt)) {
+              mine[(tv0 + dv) * c.nt + tu0 + du] += __popc(m);
+              sm[cc_] = 0u;
+            }
+          }
+      __syncwarp();
+    } else if (!__any_sync(0xffffffffu, act && (ntu > 8 || ntv > 4))) {
+      // cells (du, dv) of the rectangle at bit 8 dv + du: rectangles up to 8 x 4 tiles
+      unsigned pend = 0;
+      if (act) {
+        const unsigned row = (0x1feu << (ntu - 1)) >> 8;   // the ntu low bits
+        for (int r = 0; r < ntv; ++r) pend |= row << (8 * r);
+      }
+      if (pixmask)
+        for (int n = 0; n < 32; ++n)
+          if (((pend >> n) & 1u) && !kept(tu0 + (n & 7), tv0 + (n >> 3))) pend &= ~(1u << n);
+      for (;;) {
+        const unsigned lead = __ballot_sync(0xffffffffu, pend != 0);
+        if (!lead) break;
+        const int L = __ffs(lead) - 1;
+        const int cl = __ffs(pend) - 1;   // the leader's first pending cell (garbage elsewhere)
+        const int tup = __shfl_sync(0xffffffffu, tu0 + (cl & 7), L);
+        const int tvp = __shfl_sync(0xffffffffu, tv0 + (cl >> 3), L);
+        const unsigned du = (unsigned)(tup - tu0), dv = (unsigned)(tvp - tv0);
+        const int cell = (int)(8 * dv + du);
+        const bool in = act && du < (unsigned)ntu && dv < (unsigned)ntv && ((pend >> cell) & 1u);
+        const unsigned m = __ballot_sync(0xffffffffu, in);
+        const int t = tvp * c.nt + tup;
+        const int cur = mine[t];
+        if (in) {
+          put(cur + __popc(m & lt), j, key);
+          pend &= ~(1u << cell);
         }
         __syncwarp();
-        if (active && rank == 0) mine[t] += __popc(m);
+        if (lane == L) mine[t] = cur + __popc(m);
+        __syncwarp();
+      }
+    } else {
+      unsigned todo = __ballot_sync(0xffffffffu, act);
+      while (todo) {
+        const int L = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int a0 = __shfl_sync(0xffffffffu, tu0, L), b0 = __shfl_sync(0xffffffffu, tv0, L);
+        const int na_ = __shfl_sync(0xffffffffu, ntu, L), nb_ = __shfl_sync(0xffffffffu, ntv, L);
+        const unsigned kL = __shfl_sync(0xffffffffu, key, L);
+        const float pu = __shfl_sync(0xffffffffu, ucen, L), pv = __shfl_sync(0xffffffffu, vcen, L);
+        const float pa = __shfl_sync(0xffffffffu, ca, L), pb = __shfl_sync(0xffffffffu, cb, L);
+        const float pc = __shfl_sync(0xffffffffu, cc, L), pt = __shfl_sync(0xffffffffu, tq, L);
+        const int plo = __shfl_sync(0xffffffffu, ulo, L), phi = __shfl_sync(0xffffffffu, uhi, L);
+        const int qlo = __shfl_sync(0xffffffffu, vlo, L), qhi = __shfl_sync(0xffffffffu, vhi, L);
+        for (int n = lane; n < na_ * nb_; n += 32) {
+          const int tv = b0 + n / na_, tu = a0 + n % na_;
+          if (pixmask && !tile_kept(pu, pv, pa, pb, pc, pt, max(plo, tu << c.tshift), min(phi, (tu << c.tshift) + c.T - 1),
+                                    max(qlo, tv << c.tshift), min(qhi, (tv << c.tshift) + c.T - 1)))
+            continue;
+          const int t = tv * c.nt + tu;
+          put(mine[t]++, j0 + L, kL);
+        }
         __syncwarp();
       }
     }
@@ -542,9 +630,9 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
 
 }  // namespace
 
-void launch_prep(const CfgDev &c, const float4 *log_scale, const float4 *quat, GaussPrep *prep, DevStats *st,
-                 cudaStream_t s, int &launches) {
-  k_prep<<<(c.N + 255) / 256, 256, 0, s>>>(c.N, log_scale, quat, prep, st);
+void launch_prep(const CfgDev &c, const float4 *mean_rho, const float4 *log_scale, const float4 *quat, GaussPrep *prep,
+                 DevStats *st, cudaStream_t s, int &launches) {
+  k_prep<<<(c.N + 255) / 256, 256, 0, s>>>(c.N, mean_rho, log_scale, quat, prep, st);
   ++launches;
 }
 

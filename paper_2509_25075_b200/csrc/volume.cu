@@ -69,15 +69,20 @@ __global__ void __launch_bounds__(256) k_vol_prep(int N, const float4 *__restric
     }
     const double mu[3] = {m4.x, m4.y, m4.z};
     const double half = (double)(Dv / 2);
+    // degenerate as in the step's prep (oracle O1, reading L18): Sigma, |Sigma|, mu, rho finite
+    bool fin = isfinite(exp(dm(2.0, da(da((double)ss.x, (double)ss.y), (double)ss.z)))) && isfinite(m4.x) &&
+               isfinite(m4.y) && isfinite(m4.z) && isfinite(m4.w);
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
       const double saa = da(da(dm(dm(R[3 * ax], e[0]), R[3 * ax]), dm(dm(R[3 * ax + 1], e[1]), R[3 * ax + 1])),
                             dm(dm(R[3 * ax + 2], e[2]), R[3 * ax + 2]));
+      fin = fin && isfinite(saa);
       const double rr = dm(kk, sqrt(saa));
       lo[ax] = clip_d(ceil(da(dv(dsb(mu[ax], rr), vs), half)), 0, Dv);
       hi[ax] = clip_d(floor(da(dv(da(mu[ax], rr), vs), half)), -1, Dv - 1);
     }
-    ok = isfinite(inv[0]) && isfinite(inv[3]) && isfinite(inv[5]) && lo[0] <= hi[0] && lo[1] <= hi[1] && lo[2] <= hi[2];
+    ok = fin && isfinite(inv[0]) && isfinite(inv[3]) && isfinite(inv[5]) && lo[0] <= hi[0] && lo[1] <= hi[1] &&
+         lo[2] <= hi[2];
     r.a = m4;
     r.b = make_float4((float)inv[0], (float)inv[1], (float)inv[2], (float)inv[3]);
     r.c = make_float4((float)inv[4], (float)inv[5], __int_as_float(lo[0] | (hi[0] << 16)),

@@ -105,3 +105,40 @@ def test_volume_masked_tail_and_additivity(orc):
     a = orc.volume(tuple(p[:3] for p in params), Dv, vs)
     b = orc.volume(tuple(p[3:] for p in params), Dv, vs)
     assert np.abs(a + b - msk).max() < 1e-14 * np.abs(msk).max()
+
+
+def test_volume_box_is_tightest_ellipsoid_box(orc):
+    """O12 pin (both sides of the box): a single Gaussian's masked volume is non-zero exactly on
+    the integer voxel box of its k = 3 ellipsoid {d : d^T Sigma^-1 d <= 9}.  The ellipsoid's
+    axis extents come from an independent parametric sampling of its surface (scipy rotation,
+    numpy Cholesky): mu + 3 L u over unit vectors u.  A box that is too small (voxels of the
+    ellipsoid box missing) or too large (extra voxels) both fail."""
+    from scipy.spatial.transform import Rotation
+    rng = np.random.default_rng(12)
+    Dv, vs, k = 24, 1.1, 3.0
+    # unit vectors on a fine sphere grid: the sampled extreme is within ~1e-6 of the true one
+    th, ph = np.meshgrid(np.linspace(0, np.pi, 801), np.linspace(0, 2 * np.pi, 1601), indexing="ij")
+    U = np.stack([np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th)]).reshape(3, -1)
+    checked = 0
+    for _ in range(12):
+        mu = rng.uniform(-4, 4, 3)
+        s = np.log(rng.uniform(0.5, 2.2, 3))
+        q = rng.standard_normal(4)
+        R = Rotation.from_quat([q[1], q[2], q[3], q[0]]).as_matrix()
+        S = R @ np.diag(np.exp(2 * s)) @ R.T
+        pts = mu[:, None] + k * np.linalg.cholesky(S) @ U
+        lo = pts.min(1) / vs + Dv // 2
+        hi = pts.max(1) / vs + Dv // 2
+        if np.any(np.abs(lo - np.round(lo)) < 1e-4) or np.any(np.abs(hi - np.round(hi)) < 1e-4):
+            continue   # a bound this close to an integer cannot be decided by sampling
+        elo = np.clip(np.ceil(lo), 0, Dv).astype(int)
+        ehi = np.clip(np.floor(hi), -1, Dv - 1).astype(int)
+        vol = orc.volume(one(mu, s, q, 1.0), Dv, vs, masked=True)   # [c][b][a], x = a fastest
+        nz = np.nonzero(vol)
+        got_lo = [nz[2].min(), nz[1].min(), nz[0].min()]
+        got_hi = [nz[2].max(), nz[1].max(), nz[0].max()]
+        assert got_lo == list(elo) and got_hi == list(ehi), (got_lo, got_hi, elo, ehi)
+        # and the support is the full box (no holes: exp(-Q/2) > 0 in fp64 for Q <= ~1400)
+        assert len(nz[0]) == np.prod(ehi - elo + 1)
+        checked += 1
+    assert checked >= 8

@@ -400,3 +400,22 @@ def test_lists_pixmask_brute_force(orc):
             assert set(got) <= set(full)
             fewer += len(full) - len(got)
     assert fewer > 0   # some AABB-corner tiles hold no ellipse pixel
+
+
+def test_project_pixels_equals_full_projection(orc):
+    """orc_project_pixels (the checker of the full-size sampled GPU tests) returns, pixel by
+    pixel, the value orc_project's full image holds there: masked and un-masked, at sampled
+    pixels including image corners, box edges and pixels outside every box.  orc_project itself
+    is pinned by the mass, symmetry, quadrature and tail-bound tests above."""
+    rng = np.random.default_rng(77)
+    D, px, N = 40, 1.3, 120
+    params = _random_case(rng, N, D, px, sig_px=(0.6, 2.5), spread=0.6)
+    for s in range(3):
+        rot = Rotation.random(random_state=300 + s).as_matrix().reshape(1, 9)
+        sh = rng.uniform(-3, 3, (1, 2))
+        pix = np.concatenate([rng.integers(0, D, (200, 2)), [[0, 0], [D - 1, D - 1], [0, D - 1], [D // 2, D // 2]]])
+        for masked in (True, False):
+            full = orc.project(params, rot, sh, D, px, masked=masked)[0]
+            got = orc.project_pixels(params, rot[0], sh[0], D, px, pix, masked=masked)
+            ref = full[pix[:, 1], pix[:, 0]]
+            assert np.abs(got - ref).max() <= 1e-15 * max(np.abs(full).max(), 1e-300)
