@@ -50,7 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-o", tmp, *sources(), *LINK]
+    extra = os.environ.get("GEM_NVCC_EXTRA", "").split()   # experiment-only -D switches
+    cmd = [NVCC, *NVCC_FLAGS, *extra, "-o", tmp, *sources(), *LINK]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -107,11 +107,12 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.base = take(sizeof(int) * ((size_t)L.n_hist + 1));
   L.scan_blk = take(sizeof(unsigned long long) * ((size_t)L.n_scan_blk + 1));   // scan look-back state
   L.ids = take(sizeof(int) * (size_t)L.list_cap);
-  L.proj = take(sizeof(float) * W * D * D);
+  // + one zeroed row pair: the backward reads one pair below a box (render.cu k_render_bwd)
+  L.proj = take(sizeof(float) * (W * D * D + 2 * D));
   L.spec_hat = take(sizeof(float2) * W * H);
   L.spec_obs = take(sizeof(float2) * W * H);
   L.spec_pred = take(sizeof(float2) * W * H);
-  L.dldi = take(sizeof(float) * W * D * D);
+  L.dldi = take(sizeof(float) * (W * D * D + 2 * D));
   L.slots = take(sizeof(float) * 10 * (size_t)bwd_chunks((int)W) * N);   // backward world-frame sums [chunk][10][j]
   L.acc = take(sizeof(float4) * 3 * N);
   L.loss_part = take(sizeof(double) * Bm * (size_t)L.loss_blocks);

@@ -441,10 +441,16 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
 // registers), and the chunk's ten sums go to slot (chunk, j) (coalesced, one writer); k_bwd_reduce adds the
 // chunks in a fixed order: deterministic, no atomics, 10 floats per (chunk, j) of traffic
 // instead of 6 per (i, j).
+#ifndef GEM_BWD_UNROLL4
+#define GEM_BWD_UNROLL4 0
+#endif
+#ifndef GEM_BWD_MINB
+#define GEM_BWD_MINB 4
+#endif
 constexpr int kBwdBlock = 256, kBwdP = 8;   // threads per block, particles per thread
 
-template <bool MK>
-__global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, const SplatRec *__restrict__ rec,
+template <bool MK, int DT>   // DT: the image edge as a compile-time constant (0: c.D at run time)
+__global__ void __launch_bounds__(kBwdBlock, GEM_BWD_MINB) k_render_bwd(CfgDev c, int B, const SplatRec *__restrict__ rec,
                                                           const float *__restrict__ dldi,
                                                           const float *__restrict__ rot, float *__restrict__ slots) {
   constexpr float nh = -0.5f * kLog2e;
@@ -464,8 +470,7 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
 #pragma unroll 1
   for (int p = 0; p < np; ++p) {
   const int i = i0 + p;
-  const size_t ij = (size_t)i * c.N + j;
-  const SplatRec rr = rec[ij];
+  const SplatRec rr = rec[(size_t)i * c.N + j];
   const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
   const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
   if (ulo > uhi || vlo > vhi) continue;   // culled: contributes nothing
@@ -481,7 +486,8 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
   // MK: keep a pixel iff e >= ethr (= thr / |amp|, see keep_thr)
   const float ethr = MK ? keep_thr(c, amp, ex2(nh * c.k * c.k)) / fabsf(amp) : 0.f;
   // dL/dI in row-pair interleaved layout (k_dldi_pack): pair m, column u holds (g[2m][u], g[2m+1][u])
-  const float *gi = dldi + (size_t)i * c.D * c.D + ((size_t)(vlo >> 1) * c.D + ulo) * 2;
+  const int Dd = DT ? DT : c.D;
+  const float *gi = dldi + (size_t)i * Dd * Dd + ((size_t)(vlo >> 1) * Dd + ulo) * 2;
   // Per row the pixel weights h_k (k = 0 .. wd-1) are summed by three running sums,
   // C += h, Q += C, Z += Q (one packed op each instead of forming h k and h k^2): at the end of
   // the row C = sum h, Q = sum h t, Z = sum h t (t + 1) / 2 with t = wd - k, from which
@@ -512,13 +518,15 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
   const float2 *g0 = reinterpret_cast<const float2 *>(gi);
   if (!slow) {
     // two row pairs per iteration (independent chains: twice the loads in flight); rows outside
-    // the box carry E = 0, and a pair wholly below the box re-reads the first pair's memory
+    // the box carry E = 0.  The second pair is always read one pair below the first (a constant
+    // offset); when it lies wholly below the box its update is predicated off (its memory is
+    // valid: the next image's rows, or the buffer's one-pair pad after the last image)
     auto adv = [&]() { El *= V; V *= W; Rl *= Kb; };
 #pragma unroll 1
     for (int r = -(vlo & 1); r < ht; r += 4) {
       const bool a0 = r >= 0, b0 = r + 1 < ht, a1 = r + 2 < ht, b1 = r + 3 < ht;
-      const float2 *gp0 = g0 + (size_t)((r + (vlo & 1)) >> 1) * c.D;
-      const float2 *gp1 = a1 ? gp0 + c.D : gp0;
+      const float2 *gp0 = g0 + (size_t)((r + (vlo & 1)) >> 1) * Dd;
+      const float2 *gp1 = gp0 + Dd;
       float2 E0, R0, E1, R1;
       E0.x = a0 ? El : 0.f; R0.x = a0 ? Rl : 0.f; if (a0) adv();
       E0.y = b0 ? El : 0.f; R0.y = b0 ? Rl : 0.f; if (b0) adv();
@@ -529,7 +537,7 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
         const float2 Ea = MK ? make_float2(E0.x >= ethr ? E0.x : 0.f, E0.y >= ethr ? E0.y : 0.f) : E0;
         const float2 Eb = MK ? make_float2(E1.x >= ethr ? E1.x : 0.f, E1.y >= ethr ? E1.y : 0.f) : E1;
         C0 = __ffma2_rn(ga, Ea, C0);   // C += h, h = g e
-        C1 = __ffma2_rn(gb, Eb, C1);
+        if (a1) C1 = __ffma2_rn(gb, Eb, C1);
         Q0 = __fadd2_rn(Q0, C0);
         Q1 = __fadd2_rn(Q1, C1);
         Z0 = __fadd2_rn(Z0, Q0);
@@ -539,19 +547,38 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
         R0 = __fmul2_rn(R0, S2);
         R1 = __fmul2_rn(R1, S2);
       };
-      // column pairs at even absolute columns are read with one 128-bit load (two columns of the
-      // row pair); an odd first column and an odd last column are peeled
+      // column pairs at even absolute columns are read with 128-bit loads (two columns of the
+      // row pair), four columns per iteration; an odd first column and the last one to three
+      // columns are peeled
       int k = 0;
       if (ulo & 1) {
         step(__ldg(gp0), __ldg(gp1));
         k = 1;
       }
+#if GEM_BWD_UNROLL4
+#pragma unroll 1
+      for (; k + 3 < wd; k += 4) {
+        const float4 ga = __ldg(reinterpret_cast<const float4 *>(gp0 + k));
+        const float4 gb = __ldg(reinterpret_cast<const float4 *>(gp1 + k));
+        const float4 gc = __ldg(reinterpret_cast<const float4 *>(gp0 + k + 2));
+        const float4 gd = __ldg(reinterpret_cast<const float4 *>(gp1 + k + 2));
+        step(make_float2(ga.x, ga.y), make_float2(gb.x, gb.y));
+        step(make_float2(ga.z, ga.w), make_float2(gb.z, gb.w));
+        step(make_float2(gc.x, gc.y), make_float2(gd.x, gd.y));
+        step(make_float2(gc.z, gc.w), make_float2(gd.z, gd.w));
+      }
+      if (k + 1 < wd) {
+#else
 #pragma unroll 1
       for (; k + 1 < wd; k += 2) {
+#endif
         const float4 ga = __ldg(reinterpret_cast<const float4 *>(gp0 + k));
         const float4 gb = __ldg(reinterpret_cast<const float4 *>(gp1 + k));
         step(make_float2(ga.x, ga.y), make_float2(gb.x, gb.y));
         step(make_float2(ga.z, ga.w), make_float2(gb.z, gb.w));
+#if GEM_BWD_UNROLL4
+        k += 2;
+#endif
       }
       if (k < wd) step(__ldg(gp0 + k), __ldg(gp1 + k));
       const float dyA = dy0 + (float)r;
@@ -563,7 +590,7 @@ __global__ void __launch_bounds__(kBwdBlock, 4) k_render_bwd(CfgDev c, int B, co
     for (int r = -(vlo & 1); r < ht; r += 2) {   // direct evaluation, exp per pixel, (C, Q, Z) form
       const bool vA = r >= 0, vB = r + 1 < ht;
       const float dyA = dy0 + (float)r, dyB = dyA + 1.f;
-      const float2 *gp = g0 + (size_t)((r + (vlo & 1)) >> 1) * c.D;
+      const float2 *gp = g0 + (size_t)((r + (vlo & 1)) >> 1) * Dd;
       float2 C = make_float2(0.f, 0.f), Q = C, Z = C;
       const float fA = fmaf(dyA, fmaf(nc, dyA, Gx), Fx), fB = fmaf(dyB, fmaf(nc, dyB, Gx), Fx);
       const float gA = fmaf(nb2, dyA, D0), gB = fmaf(nb2, dyB, D0);
@@ -708,8 +735,11 @@ int bwd_chunks(int B) { return (B + kBwdP - 1) / kBwdP; }
 void launch_render_bwd(const CfgDev &c, int B, const SplatRec *rec, const float *dldi, const float *rot, float *slots,
                        cudaStream_t s, int &launches) {
   dim3 grid((c.N + kBwdBlock - 1) / kBwdBlock, bwd_chunks(B));
-  if (pixel_mask(c)) k_render_bwd<true><<<grid, kBwdBlock, 0, s>>>(c, B, rec, dldi, rot, slots);
-  else k_render_bwd<false><<<grid, kBwdBlock, 0, s>>>(c, B, rec, dldi, rot, slots);
+  const bool mk = pixel_mask(c);
+  auto go = [&](auto kern) { kern<<<grid, kBwdBlock, 0, s>>>(c, B, rec, dldi, rot, slots); };
+  if (c.D == 256) mk ? go(k_render_bwd<true, 256>) : go(k_render_bwd<false, 256>);
+  else if (c.D == 128) mk ? go(k_render_bwd<true, 128>) : go(k_render_bwd<false, 128>);
+  else mk ? go(k_render_bwd<true, 0>) : go(k_render_bwd<false, 0>);
   ++launches;
 }
 
