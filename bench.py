@@ -33,7 +33,10 @@ from paper_2509_25075_b200 import synth  # noqa: E402
 
 METRIC = "particle images/sec per train step (fwd+bwd) at D=256"
 SNR = 0.1
-# algorithmic FP32 FLOPs per useful (Gaussian, pixel) pair (FMA = 2 FLOPs)
+# algorithmic work per useful (Gaussian, pixel) pair of the direct method (DESIGN.md
+# §5): FP32 lane-ops (an FMA counts once) -- the roofline's unit -- and FLOPs (an FMA counts twice)
+LANEOPS_FWD_PAIR = 9
+LANEOPS_BWD_PAIR = 22
 FLOP_FWD_PAIR = 12
 FLOP_BWD_PAIR = 25
 
@@ -98,6 +101,33 @@ def measured_traffic(kernel, workload, batch, tile, variant):
 def fp32_peak_tflops(sm_mhz):
     """148 SMs x 128 FP32 lanes x 2 FLOP/FMA x clock (B200_PROFILING.md unit counts)."""
     return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+def fp32_peak_tlaneops(sm_mhz):
+    """148 SMs x 128 FP32 lanes x clock: FP32 lane-operations per second (T/s)."""
+    return 148 * 128 * sm_mhz * 1e6 / 1e12
+
+
+def cpu_info():
+    """CPU model, sockets and threads of the host (lscpu), for the cpu_baseline record."""
+    info = {}
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "Model name":
+                info["cpu_model"] = v
+            elif k == "Socket(s)":
+                info["sockets"] = int(v) if v.isdigit() else v
+            elif k == "CPU(s)":
+                info["host_threads"] = int(v) if v.isdigit() else v
+            elif k == "Thread(s) per core":
+                info["threads_per_core"] = int(v) if v.isdigit() else v
+    except Exception:
+        pass
+    return info
 
 
 class ClockSampler:
@@ -190,7 +220,8 @@ def cpu_baseline(w, budget_s=15.0):
     t = oracle_step_sample(w, n) if n > 1 else t1
     return {"value": n / t, "unit": "particles/s", "cores": cpu_cores(), "kind": "oracle",
             "sample": f"{n} particle(s) of workload {w.name} (N={w.N}, D={w.D}): full fp64 forward "
-                      f"(masked sum over every Gaussian x pixel), DFT CTF/loss, backward, Adam; {t:.1f} s"}
+                      f"(masked sum over every Gaussian x pixel), DFT CTF/loss, backward, Adam; {t:.1f} s",
+            **cpu_info()}
 
 
 def run_reference(args, rank, world):
@@ -223,7 +254,7 @@ def run_reference(args, rank, world):
             "config": {"workload": f"{w.name}: N={w.N} Gaussians, D={w.D}, px={w.px} A", "batch_per_step": per_step,
                        "requested_steps": args.steps},
             "cpu_baseline": {"value": value, "unit": "particles/s", "cores": cpu_cores(), "kind": "oracle",
-                             "sample": f"{per_step} particle per step x {steps} steps"},
+                             "sample": f"{per_step} particle per step x {steps} steps", **cpu_info()},
             "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -246,7 +277,13 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # communicator set-up lines (ranks, transports: NVLink / NVLS) on stderr for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
+        if rank == 0:
+            print(f"[bench] NCCL process group: world={world} backend={dist.get_backend()} "
+                  f"nccl={torch.cuda.nccl.version()}", file=sys.stderr, flush=True)
 
     w = synth.CONFIGS[args.config]
     # weak scaling (default): B particles per GPU; strong scaling: a fixed global batch split
@@ -330,32 +367,55 @@ def main():
     st = sc.stats(check=False)
     value = world * B * args.steps / (ms / 1e3)
 
-    # ---- e2e: the same steps from pinned HOST inputs through the public API (gem.HostPipeline:
-    # every step's inputs are copied host->device on a side stream, double-buffered so that the
-    # copy of step k+1 overlaps step k, and every step's loss is read back to pinned host memory)
+    # ---- e2e: the same steps from pinned HOST inputs through the C ABI's own host path
+    # (gem_batch.memory = GEM_MEM_HOST: every call copies its poses, CTFs and observed images
+    # host->device -- the images on libgem's side stream, overlapped with the splat / binning /
+    # render -- and writes the loss to pinned host memory).  Also reported: gem.HostPipeline,
+    # which double-buffers the next step's copy behind the current step from Python.
     e2e = None
     if not args.no_e2e:
         hsrc = [a.cpu().pin_memory() for a in (rot, shift, ctf, obs)]
+        hloss = torch.empty(B + 1, dtype=torch.float64, pin_memory=True)
+        hsrc.append(hloss)
+
+        def timed(fn):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1)
+            if world > 1:
+                tt = torch.tensor([t], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            return t
+
+        for k in range(2):
+            step(k, host=True, src=hsrc)
+
+        def abi_steps():
+            for k in range(args.steps):
+                step(args.warmup + k, host=True, src=hsrc)
+        ems = timed(abi_steps)
+        _ = float(hloss[-1])  # the last step's loss, read on the host
         pipe = gem.HostPipeline(tr, B, w.D)
-        batch = lambda k: [a[((k * B) % ring):((k * B) % ring) + B] for a in hsrc]
+        batch = lambda k: [a[((k * B) % ring):((k * B) % ring) + B] for a in hsrc[:4]]
         pipe.run([batch(k) for k in range(2)])
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        lh = pipe.run([batch(args.warmup + k) for k in range(args.steps)])
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ems], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        _ = float(lh[-1])  # the last step's loss, read on the host
+        holder = {}
+        pms = timed(lambda: holder.setdefault("lh", pipe.run([batch(args.warmup + k) for k in range(args.steps)])))
+        _ = float(holder["lh"][-1])
         e2e = {"value": world * B * args.steps / (ems / 1e3), "unit": "particles/s",
                "h2d_bytes_per_step": B * (9 + 2 + 8 + w.D * w.D) * 4, "d2h_bytes_per_step": (B + 1) * 8,
-               "path": "gem.HostPipeline: pinned host -> device copies on a side stream, double-buffered"}
+               "path": "C ABI gem_forward with gem_batch.memory = GEM_MEM_HOST (pinned host poses, CTFs, "
+                       "images copied inside every call; images on libgem's side stream) + gem_backward + "
+                       "all-reduce + gem_step",
+               "host_pipeline": {"value": world * B * args.steps / (pms / 1e3), "unit": "particles/s",
+                                 "path": "gem.HostPipeline: the next step's inputs copied on a Python side "
+                                         "stream, double-buffered behind the current step"}}
 
     # Table 1's memory metric: what the training step holds on the device.  The
     # synthetic data ring is a dataset stand-in and is reported apart.
@@ -385,17 +445,30 @@ def main():
     dominant = max(kern, key=lambda k: kern[k][1]) if kern else None
     roof = None
     if dominant in ("render_fwd", "render_bwd"):
-        per_pair = FLOP_FWD_PAIR if dominant == "render_fwd" else FLOP_BWD_PAIR
+        per_pair = LANEOPS_FWD_PAIR if dominant == "render_fwd" else LANEOPS_BWD_PAIR
+        flop_pair = FLOP_FWD_PAIR if dominant == "render_fwd" else FLOP_BWD_PAIR
         avg_s = kern[dominant][1] / kern[dominant][0] / 1e3          # per launch (one wave)
-        achieved = per_pair * pairs * args.steps / (kern[dominant][1] / 1e3) / 1e12
-        peak = fp32_peak_tflops(sm_max)
-        roof = {"bound": "alu", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak,
+        sec = kern[dominant][1] / 1e3
+        achieved = per_pair * pairs * args.steps / sec / 1e12
+        peak = fp32_peak_tlaneops(sm_max)
+        roof = {"bound": "alu", "kernel": dominant, "achieved": achieved, "peak": peak,
+                "unit": "T FP32 lane-ops/s", "frac": achieved / peak,
                 "traffic": measured_traffic(dominant, args.config, B, args.tile, variant),
-                "work_per_launch": f"{per_pair} FP32 FLOP x {pairs} useful (Gaussian, pixel) pairs per step, "
-                                   f"{kern[dominant][0] // max(args.steps, 1)} launch(es) per step",
+                "work_per_launch": f"{per_pair} FP32 lane-ops (SURVEY 8(d), an FMA counted once) x {pairs} useful "
+                                   f"(Gaussian, pixel) pairs per step, {kern[dominant][0] // max(args.steps, 1)} "
+                                   "launch(es) per step",
                 "avg_launch_ms": avg_s * 1e3,
-                "peak_source": f"148 SMs x 128 FP32 lanes x 2 FLOP/FMA x {sm_max:.0f} MHz ({peak_src} sm_max_mhz)"}
+                "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz ({peak_src} sm_max_mhz)",
+                "flop_fma2": {"achieved_tflops": flop_pair * pairs * args.steps / sec / 1e12,
+                              "peak_tflops": fp32_peak_tflops(sm_max),
+                              "frac": flop_pair * pairs * args.steps / sec / 1e12 / fp32_peak_tflops(sm_max),
+                              "note": f"{flop_pair} FLOP per pair with an FMA = 2 FLOP"}}
+        other = "render_bwd" if dominant == "render_fwd" else "render_fwd"
+        if other in kern:
+            op = LANEOPS_BWD_PAIR if other == "render_bwd" else LANEOPS_FWD_PAIR
+            osec = kern[other][1] / 1e3
+            roof["other_render_kernel"] = {"kernel": other, "ms_per_step": kern[other][1] / max(args.steps, 1),
+                                           "frac": op * pairs * args.steps / osec / 1e12 / peak}
     elif dominant is not None:
         roof = {"bound": "hbm", "kernel": dominant, "achieved": None, "peak": float(peaks.get("hbm_gbs", 6650.0)),
                 "unit": "GB/s", "frac": None, "traffic": None}
@@ -463,7 +536,9 @@ def main():
                    "l2": "inputs larger than L2: per-step working set (splat records "
                          f"{B * w.N * 32 / 1e6:.0f} MB + images) and a {ring}-particle ring "
                          f"({ring * w.D * w.D * 4 / 1e6:.0f} MB) exceed the 126 MB L2",
-                   "useful_pairs_per_step": pairs, "list_entries_per_step": int(st["entries"])},
+                   "useful_pairs_per_step": pairs, "list_entries_per_step": int(st["entries"]),
+                   "list_capacity": int(st["capacity"]), "list_overflow": int(st["overflow"]),
+                   "nonfinite": int(st["nonfinite"]), "degenerate_gaussians": int(st["degenerate"])},
         "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks,
         "memory": memory, "replicas_identical": replicas, "volume": vol,
@@ -471,6 +546,11 @@ def main():
         "kernel_times": "CUDA event pair around each launch group, second pass over the same K steps",
     }
     print(json.dumps(line), flush=True)
+    if st["overflow"] or st["nonfinite"]:
+        # truncated tile lists (list capacity exceeded) or a non-finite loss: the step's outputs
+        # are invalid (include/gem.h), so the run fails instead of reporting a number
+        print(f"[bench] invalid run: list_overflow={st['overflow']} nonfinite={st['nonfinite']}", file=sys.stderr)
+        return 3
     if world > 1:
         dist.destroy_process_group()
     return 0

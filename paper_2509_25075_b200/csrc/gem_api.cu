@@ -405,9 +405,15 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
   // the rotation is kept in the workspace for gem_backward
   CK(cudaMemcpyAsync(rot, batch->rot, sizeof(float) * 9 * B, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
   if (host) {
+    // poses on the compute stream (the splat needs them first); the CTF parameters and the
+    // observed images (4 D^2 bytes per particle, the bulk of the input) on the internal side
+    // stream, where their only consumers (CTF constants, the observations' R2C) run: that copy
+    // overlaps the splat, binning and render of the compute stream
     CK(cudaMemcpyAsync(at<float>(ctx, L.stage_shift), shift, sizeof(float) * 2 * B, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(at<float>(ctx, L.stage_ctf), ctf, sizeof(float) * 8 * B, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(at<float>(ctx, L.stage_obs), obs, sizeof(float) * B * D * D, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(ctx->ev_fork, s));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    CK(cudaMemcpyAsync(at<float>(ctx, L.stage_ctf), ctf, sizeof(float) * 8 * B, cudaMemcpyHostToDevice, ctx->side));
+    CK(cudaMemcpyAsync(at<float>(ctx, L.stage_obs), obs, sizeof(float) * B * D * D, cudaMemcpyHostToDevice, ctx->side));
     shift = at<float>(ctx, L.stage_shift);
     ctf = at<float>(ctx, L.stage_ctf);
     obs = at<float>(ctx, L.stage_obs);

@@ -211,17 +211,24 @@ class Trainer:
         self.params = params
         N = params.N
         dev = params.t.device
-        self.grad = SoA.zeros(N, dev)
+        # one contiguous fp32 buffer: the [3, N, 4] gradient, then the rank's total loss (and 3
+        # pad words, keeping 16-byte alignment): SURVEY §8(a) a9's single all-reduce payload
+        self.flat = torch.zeros(12 * N + 4, dtype=torch.float32, device=dev)
+        self.grad = SoA(self.flat[: 12 * N].view(3, N, 4))
         self.m = SoA.zeros(N, dev)
         self.v = SoA.zeros(N, dev)
         self.t = 0
         self.group = group
+        self.global_loss = self.flat[12 * N: 12 * N + 1]   # sum over ranks after each step (fp32)
 
     def train_step(self, rot, shift, ctf, observed, host=False, loss=None):
         g = self.step_ctx
         loss = g.forward(self.params, rot, shift, ctf, observed, loss=loss, host=host)
         g.backward(self.params, self.grad)
-        allreduce_grad(self.grad, self.group)
+        with torch.cuda.stream(g.stream) if self.flat.is_cuda else _nullctx():
+            self.global_loss.copy_(loss[-1:], non_blocking=True)   # the rank's total, appended
+            if _world(self.group) > 1:
+                allreduce_flat(self.flat, self.group)                # gradient + loss: one collective
         self.t += 1
         g.step(self.params, self.grad, self.m, self.v, self.t)
         return loss
@@ -269,6 +276,27 @@ class HostPipeline:
             with torch.cuda.stream(self.compute):
                 self.loss_host.copy_(loss, non_blocking=True)
         return self.loss_host
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def _world(group=None) -> int:
+    import torch.distributed as dist
+    return dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+
+
+def allreduce_flat(flat: "torch.Tensor", group=None):
+    """Sum a contiguous fp32 buffer (gradient + appended loss) over the data-parallel ranks."""
+    import torch.distributed as dist
+    if _world(group) > 1:
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    return flat
 
 
 def allreduce_grad(grad: SoA, group=None):

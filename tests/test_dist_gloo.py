@@ -42,8 +42,14 @@ def _worker(rank, world, port, outdir):
     w, params, rot, shift, ctf, obs = _case()
     idx = gem.shard_indices(8, world, rank, batch=4, step=0, seed=3)
     out = oracle.loss_grad(params, rot[idx], shift[idx], ctf[idx], obs[idx], w.D, float(np.float32(w.px)))
-    g = gem.SoA(torch.from_numpy(oracle.grad_to_soa(out["grad"]).astype(np.float32)).contiguous())
-    gem.allreduce_grad(g)
+    # gem.Trainer's single payload: the [3, N, 4] gradient, then the rank's total loss, then pad
+    N = params[0].shape[0]
+    flat = torch.zeros(12 * N + 4, dtype=torch.float32)
+    flat[: 12 * N] = torch.from_numpy(oracle.grad_to_soa(out["grad"]).astype(np.float32)).reshape(-1)
+    flat[12 * N] = float(out["total"])
+    gem.allreduce_flat(flat)
+    g = gem.SoA(flat[: 12 * N].view(3, N, 4))
+    np.save(os.path.join(outdir, f"loss{rank}.npy"), flat[12 * N:].numpy())
     p = np.stack(params).astype(np.float64)
     p1, _, _ = oracle.adam(p, g.t.numpy().astype(np.float64), np.zeros_like(p), np.zeros_like(p), 1,
                            [1e-3, 5e-3, 1e-3, 5e-2])
@@ -82,5 +88,7 @@ def test_gloo_allreduce_equals_full_batch(tmp_path, orc):
     g0, g1 = np.load(tmp_path / "g0.npy"), np.load(tmp_path / "g1.npy")
     assert np.array_equal(g0, g1)                    # every rank holds identical reduced bytes
     assert np.abs(g0 - ref).max() <= 1e-6 * np.abs(ref).max()
+    l0 = np.load(tmp_path / "loss0.npy")
+    assert abs(l0[0] - full["total"]) <= 1e-6 * full["total"] and np.all(l0[1:] == 0)   # loss summed alongside
     h0 = np.load(tmp_path / "h0.npy")
     assert h0[0] and not h0[1]                        # replicated Adam stays bit-identical; a 1-ulp drift is caught
