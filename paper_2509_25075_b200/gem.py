@@ -99,7 +99,9 @@ def _ptr(t):
 class GemStep:
     """Owns one libgem context, its workspace (a torch uint8 tensor) and stream."""
 
-    def __init__(self, cfg: GemConfig, device=None, stream: torch.cuda.Stream | None = None):
+    def __init__(self, cfg: GemConfig, device=None, stream: torch.cuda.Stream | None = None, guard_bytes: int = 0):
+        """guard_bytes > 0 (tests): that many canary bytes (0xA5) follow the workspace; see
+        guard_intact()."""
         self.cfg = cfg
         self.device = torch.device(device or "cuda")
         self.lib = _b.lib()
@@ -108,15 +110,23 @@ class GemStep:
         nbytes = self.lib.gem_workspace_bytes(ctypes.byref(c))
         if nbytes == 0:
             raise _b.GemError(_b.GEM_E_INVALID, "gem_workspace_bytes")
-        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        self.workspace = torch.empty(nbytes + 256 + guard_bytes, dtype=torch.uint8, device=self.device)
         off = (-self.workspace.data_ptr()) % 256
         self._ws_ptr = self.workspace.data_ptr() + off
         self._ws_bytes = nbytes
+        self._guard = self.workspace[off + nbytes: off + nbytes + guard_bytes] if guard_bytes else None
+        if self._guard is not None:
+            self._guard.fill_(0xA5)
         h = ctypes.c_void_p()
         _b.check(self.lib.gem_init(ctypes.byref(c), self._ws_ptr, nbytes, self.stream.cuda_stream, ctypes.byref(h)),
                  "gem_init")
         self.ctx = h
         self.launches = 0
+
+    def guard_intact(self) -> bool:
+        """True if no kernel wrote past the end of the workspace (the canary bytes are intact)."""
+        torch.cuda.synchronize(self.device)
+        return self._guard is None or bool((self._guard == 0xA5).all())
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -161,12 +171,18 @@ class GemStep:
         if out is None:
             out = torch.empty((Dv, Dv, Dv), dtype=torch.float32, device=self.device)
         nbytes = self.lib.gem_volume_scratch_bytes(self.ctx, Dv, voxel_size)
-        scratch = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
-        ptr = scratch.data_ptr() + ((-scratch.data_ptr()) % 256)
+        gb = 4096 if self._guard is not None else 0
+        scratch = torch.empty(nbytes + 256 + gb, dtype=torch.uint8, device=self.device)
+        off = (-scratch.data_ptr()) % 256
+        ptr = scratch.data_ptr() + off
+        if gb:
+            scratch[off + nbytes: off + nbytes + gb].fill_(0xA5)
         sp = params.c()
         _b.check(self.lib.gem_render_volume(self.ctx, ctypes.byref(sp), Dv, voxel_size, out.data_ptr(), ptr, nbytes,
                                             self.stream.cuda_stream), "gem_render_volume")
         self.launches += self.lib.gem_last_launch_count(self.ctx)
+        if gb and not bool((scratch[off + nbytes: off + nbytes + gb] == 0xA5).all()):
+            raise RuntimeError("gem_render_volume wrote past its scratch buffer")
         return out
 
     def export_lists(self, particle: int):
