@@ -20,6 +20,17 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   return y;
 }
 
+// Rounding on the FMA/ALU pipes instead of the XU (FRND / F2I run at 16 lanes/clk/SM): for
+// |x| < 2^22, x + 1.5 * 2^23 rounds x to the nearest integer in the low mantissa bits.
+constexpr float kMagicF = 12582912.f;      // 1.5 * 2^23
+constexpr int kMagicBits = 0x4B400000;
+__device__ __forceinline__ float rint_fma(float x) { return __fsub_rn(__fadd_rn(x, kMagicF), kMagicF); }
+__device__ __forceinline__ int iround_fma(float x) { return __float_as_int(__fadd_rn(x, kMagicF)) - kMagicBits; }
+// exact int -> double (|i| < 2^31) by the 2^52 + 2^51 magic: one DADD, no I2F.F64
+__device__ __forceinline__ double i2d_magic(int i) {
+  return __dsub_rn(__hiloint2double(0x43380000, i ^ 0x80000000), 6755401588539392.0);   // 2^52 + 2^51 + 2^31
+}
+
 __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsb(double a, double b) { return __dsub_rn(a, b); }
@@ -194,8 +205,18 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
       const int tu0 = (ulo >> c.tshift), tu1 = (uhi >> c.tshift), tv0 = (vlo >> c.tshift), tv1 = (vhi >> c.tshift);
       int *sub = shist + ((j - ch * kChunk) / kSub) * c.NT;
       if (!pixmask) {
-        for (int tv = tv0; tv <= tv1; ++tv)
-          for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&sub[tv * c.nt + tu], 1);
+        if (tu1 - tu0 <= 1 && tv1 - tv0 <= 1) {   // the usual case: a 1x1 .. 2x2 tile rectangle
+          int *h0 = sub + tv0 * c.nt + tu0;
+          atomicAdd(h0, 1);
+          if (tu1 > tu0) atomicAdd(h0 + 1, 1);
+          if (tv1 > tv0) {
+            atomicAdd(h0 + c.nt, 1);
+            if (tu1 > tu0) atomicAdd(h0 + c.nt + 1, 1);
+          }
+        } else {
+          for (int tv = tv0; tv <= tv1; ++tv)
+            for (int tu = tu0; tu <= tu1; ++tu) atomicAdd(&sub[tv * c.nt + tu], 1);
+        }
       } else {   // per-pixel selection: only tiles holding a kept pixel (exact ellipse-tile test)
         const float tq = keep_q(c, ampf), ucen = (float)ulo + mxp, vcen = (float)vlo + myp;
         for (int tv = tv0; tv <= tv1; ++tv)
@@ -246,23 +267,28 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
     // fp32 error here is < 1e-4 px (positive sums, fp64 centre): a floor/ceil is certain unless
     // the value lies within 1e-3 px of an integer (or anything looks degenerate) -> exact queue
     const float e = 1e-3f;
-    const bool okf = s3[0] >= 0.f && d2f > 0.f && fabsf(ampf) < 3e38f && fabsf(fu0) < 1e9f && fabsf(fu1) < 1e9f &&
-                     fabsf(fv0) < 1e9f && fabsf(fv1) < 1e9f;
-    const bool near = fabsf(fu0 - rintf(fu0)) < e || fabsf(fu1 - rintf(fu1)) < e || fabsf(fv0 - rintf(fv0)) < e ||
-                      fabsf(fv1 - rintf(fv1)) < e || (tau > 0.0 && fabsf(fabsf(ampf) - tauf) <= 1e-4f * tauf);
+    // |bounds| < 2^21 keeps the magic-number rounding exact (the clip below goes to [-1, D])
+    const bool okf = s3[0] >= 0.f && d2f > 0.f && fabsf(ampf) < 3e38f && fabsf(fu0) < 2e6f && fabsf(fu1) < 2e6f &&
+                     fabsf(fv0) < 2e6f && fabsf(fv1) < 2e6f;
+    const float ru0 = rint_fma(fu0), ru1 = rint_fma(fu1), rv0 = rint_fma(fv0), rv1 = rint_fma(fv1);
+    const bool near = fabsf(fu0 - ru0) < e || fabsf(fu1 - ru1) < e || fabsf(fv0 - rv0) < e || fabsf(fv1 - rv1) < e ||
+                      (tau > 0.0 && fabsf(fabsf(ampf) - tauf) <= 1e-4f * tauf);
     if (s3[0] >= 0.f && (!okf || near)) {   // deferred to the exact pass (compact, no warp divergence)
       queue[atomicAdd(&qn, 1)] = j;
       continue;
     }
-    // clip as the canonical chain does: lo to [0, D], hi to [-1, D-1] (in float: no overflow)
-    const int ulo = (int)fminf(fmaxf(ceilf(fu0), 0.f), Df);
-    const int uhi = (int)fmaxf(fminf(floorf(fu1), Df - 1.f), -1.f);
-    const int vlo = (int)fminf(fmaxf(ceilf(fv0), 0.f), Df);
-    const int vhi = (int)fmaxf(fminf(floorf(fv1), Df - 1.f), -1.f);
+    // not near an integer: ceil(x) = rint(x) + (rint(x) < x), floor(x) = rint(x) - (rint(x) > x);
+    // clip as the canonical chain does: lo to [0, D], hi to [-1, D-1]
+    const float cu0 = ru0 + (ru0 < fu0 ? 1.f : 0.f), fu1f = ru1 - (ru1 > fu1 ? 1.f : 0.f);
+    const float cv0 = rv0 + (rv0 < fv0 ? 1.f : 0.f), fv1f = rv1 - (rv1 > fv1 ? 1.f : 0.f);
+    const int ulo = iround_fma(fminf(fmaxf(cu0, 0.f), Df));
+    const int uhi = iround_fma(fmaxf(fminf(fu1f, Df - 1.f), -1.f));
+    const int vlo = iround_fma(fminf(fmaxf(cv0, 0.f), Df));
+    const int vhi = iround_fma(fmaxf(fminf(fv1f, Df - 1.f), -1.f));
     const bool vis = okf && fabsf(ampf) > tauf && ulo <= uhi && vlo <= vhi;
     const float id2 = px2f / d2f;
-    emit(j, vis, ulo, uhi, vlo, vhi, (float)(mxd - (double)ulo), (float)(myd - (double)vlo), Cf * id2, -Bf * id2,
-         Af * id2, ampf);
+    emit(j, vis, ulo, uhi, vlo, vhi, (float)__dsub_rn(mxd, i2d_magic(ulo)), (float)__dsub_rn(myd, i2d_magic(vlo)),
+         Cf * id2, -Bf * id2, Af * id2, ampf);
   }
   __syncthreads();
   for (int k = tid; k < qn; k += blockDim.x) {   // exact pass over the deferred Gaussians
