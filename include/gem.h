@@ -72,7 +72,9 @@ typedef enum {
 
 /* Host struct, copied at gem_init. */
 typedef struct {
-  int32_t D;              /* image edge in pixels, even, >= 2               */
+  int32_t D;              /* image edge in pixels, even, >= 2; the tile grid
+                             must fit the binning's shared-memory histograms: D <= 856
+                             with 8x8 tiles, D <= 1712 with 16x16 (else GEM_E_INVALID)    */
   float pixel_size;       /* Angstrom per pixel, > 0                                      */
   int64_t n_gauss;        /* N Gaussians (the paper's M), >= 1               */
   int32_t max_batch;      /* max particles per gem_forward, >= 1                          */

@@ -53,6 +53,10 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   } else {
     c.wave = c.max_batch;
   }
+  // the splat kernel keeps kFillWarps tile histograms plus a kChunk exact queue in shared memory
+  // and the fill kFillWarps cursor arrays: the tile grid must fit (D <= 856 at 8x8 tiles,
+  // D <= 1712 at 16x16)
+  if ((size_t)(4 * d.NT + kChunk) * sizeof(int) > 200 * 1024) return false;
   if (c.list_capacity <= 0)   // per wave (= per batch when not fused)
     c.list_capacity = (int64_t)c.wave * ((c.tile == 16 ? 6 : 12) * (int64_t)d.N + d.NT);
   if (c.list_capacity > 0x7fffffffll) c.list_capacity = 0x7fffffffll;
@@ -429,7 +433,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
   float4 *acc = at<float4>(ctx, L.acc);
   double *lpart = at<double>(ctx, L.loss_part);
   if (ctx->fused) CK(cudaMemsetAsync(acc, 0, sizeof(float4) * 3 * (size_t)c.N, s));
-  { Prof p(ctx, s, P_PREP); launch_prep(c, (const float4 *)params->mean_rho, (const float4 *)params->log_scale, (const float4 *)params->quat, prep, st, s, ctx->launches); }
+  { Prof p(ctx, s, P_PREP); launch_prep(c, (const float4 *)params->mean_rho, (const float4 *)params->log_scale, (const float4 *)params->quat, prep, st, s, ctx->launches); CK(cudaGetLastError()); }
   const size_t DD = D * D;
   int p0 = 0, nb = 0;
   for (p0 = 0; p0 < B; p0 += ctx->W) {   // one wave (all of B when not fused)
@@ -447,27 +451,29 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
       Prof p(ctx, ctx->side, P_FFT_OBS);
       CKF(cufftExecR2C(r2c_obs, (cufftReal *)(obs + p0 * DD), (cufftComplex *)so));
     }
-    { Prof p(ctx, ctx->side, P_CTF_LOSS); launch_ctf_params(c, nb, ctf + 8 * (size_t)p0, ctx->ws + L.ctf_par, ctx->side, ctx->launches); }
+    { Prof p(ctx, ctx->side, P_CTF_LOSS); launch_ctf_params(c, nb, ctf + 8 * (size_t)p0, ctx->ws + L.ctf_par, ctx->side, ctx->launches); CK(cudaGetLastError()); }
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
     const float *rw = rot + 9 * (size_t)p0;
     { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist, at<int>(ctx, L.subcnt), st, s,
-                         ctx->launches); }
+                         ctx->launches); CK(cudaGetLastError()); }
     const int64_t nh = (int64_t)nb * c.NT * c.C;
     {
       Prof p(ctx, s, P_SCAN);
       launch_scan_1p(hist, base, nh, at<unsigned long long>(ctx, L.scan_blk), (nh + 4095) / 4096,
                      ctx->scan_epoch = ctx->scan_epoch % 0x3ffffffeu + 1u,   // 1 .. 2^30 - 1 (state zeroed at init)
                      at<int>(ctx, L.ticket) + 8, st, c.cap, s, ctx->launches);
+      CK(cudaGetLastError());
     }
     uint2 *zpair = (c.flags & GEM_FLAG_ZSORT) ? at<uint2>(ctx, L.zs_key) : nullptr;
-    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<int>(ctx, L.subcnt), ids, (const float4 *)params->mean_rho, rw, zpair, rec, s, ctx->launches); }
+    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<int>(ctx, L.subcnt), ids, (const float4 *)params->mean_rho, rw, zpair, rec, s, ctx->launches); CK(cudaGetLastError()); }
     if (zpair) {
       Prof p(ctx, s, P_ZSORT);
       launch_zsort(c, nb, base, (const float4 *)params->mean_rho, rw, ids, zpair, at<int>(ctx, L.zs_tmp),
                    at<int>(ctx, L.zs_queue), s, ctx->launches);
+      CK(cudaGetLastError());
     }
     float *proj = proj_out ? proj_out + p0 * DD : at<float>(ctx, L.proj);
-    { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, base, ids, proj, at<int>(ctx, L.ticket), s, ctx->launches); }
+    { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, base, ids, proj, at<int>(ctx, L.ticket), s, ctx->launches); CK(cudaGetLastError()); }
     CKF(cufftSetStream(r2c, s));
     CKF(cufftSetStream(c2r, s));
     {
@@ -480,6 +486,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
       launch_ctf_loss(c, nb, ctx->ws + L.ctf_par, sh, so, pred_out ? sp : nullptr,
                       c2r_il ? at<float2>(ctx, L.proj) : nullptr, lpart + (size_t)p0 * L.loss_blocks,
                       L.loss_blocks, s, ctx->launches);
+      CK(cudaGetLastError());
     }
     CK(cudaEventRecord(ctx->ev_ctf, s));
     {
@@ -496,15 +503,18 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
         float *raw = at<float>(ctx, L.proj);
         CKF(cufftExecC2R(c2r, (cufftComplex *)sh, (cufftReal *)raw));
         launch_dldi_pack(c, nb, raw, dldi, s, ctx->launches);
+        CK(cudaGetLastError());
       }
     }
     if (ctx->fused) {
       {
         Prof p(ctx, s, P_RENDER_BWD);
         launch_render_bwd(c, nb, rec, dldi, rw, at<float>(ctx, L.slots), s, ctx->launches);
+        CK(cudaGetLastError());
       }
       Prof p(ctx, s, P_BWD_REDUCE);
       launch_bwd_reduce(c, nb, at<float>(ctx, L.slots), (const float4 *)params->mean_rho, acc, s, ctx->launches);
+      CK(cudaGetLastError());
     }
   }
   ctx->last_p0 = p0 - ctx->W;
@@ -513,7 +523,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
   // overlapped with the last C2R; the caller's stream joins it before anything that follows
   double *lossd = host ? at<double>(ctx, L.stage_loss) : loss;
   CK(cudaStreamWaitEvent(ctx->side, ctx->ev_ctf, 0));
-  { Prof p(ctx, ctx->side, P_CTF_LOSS); launch_loss_reduce(B, lpart, L.loss_blocks, lossd, st, at<int>(ctx, L.ticket) + 4, ctx->side, ctx->launches); }
+  { Prof p(ctx, ctx->side, P_CTF_LOSS); launch_loss_reduce(B, lpart, L.loss_blocks, lossd, st, at<int>(ctx, L.ticket) + 4, ctx->side, ctx->launches); CK(cudaGetLastError()); }
   if (host) CK(cudaMemcpyAsync(loss, lossd, sizeof(double) * (B + 1), cudaMemcpyDeviceToHost, ctx->side));
   CK(cudaEventRecord(ctx->ev_loss, ctx->side));
   CK(cudaStreamWaitEvent(s, ctx->ev_loss, 0));
@@ -538,17 +548,20 @@ gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_
       Prof p(ctx, s, P_RENDER_BWD);
       launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<float>(ctx, L.dldi), at<float>(ctx, L.stage_rot),
                         at<float>(ctx, L.slots), s, ctx->launches);
+      CK(cudaGetLastError());
     }
     Prof p(ctx, s, P_BWD_REDUCE);
     launch_reduce_finalize(c, ctx->last_B, at<float>(ctx, L.slots), at<GaussPrep>(ctx, L.prep), (const float4 *)params->mean_rho,
                            (const float4 *)params->log_scale, (const float4 *)params->quat, (float4 *)grad->mean_rho,
                            (float4 *)grad->log_scale, (float4 *)grad->quat, at<DevStats>(ctx, L.stats), s,
                            ctx->launches);
+    CK(cudaGetLastError());
   } else {   // fused mode: the forward already reduced every wave into acc
     Prof pf(ctx, s, P_FINALIZE);
     launch_finalize(c, acc, at<GaussPrep>(ctx, L.prep), (const float4 *)params->mean_rho, (const float4 *)params->log_scale,
                     (const float4 *)params->quat, (float4 *)grad->mean_rho, (float4 *)grad->log_scale,
                     (float4 *)grad->quat, at<DevStats>(ctx, L.stats), s, ctx->launches);
+    CK(cudaGetLastError());
   }
   CK(cudaGetLastError());
   return GEM_OK;

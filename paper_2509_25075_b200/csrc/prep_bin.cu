@@ -264,14 +264,19 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
     const float cx = (float)mxd, cy = (float)myd;
     const float rxp = kf * (Af * rsqrt_approx(Af)) * ipxf, ryp = kf * (Cf * rsqrt_approx(Cf)) * ipxf;
     const float fu0 = cx - rxp, fu1 = cx + rxp, fv0 = cy - ryp, fv1 = cy + ryp;
-    // fp32 error here is < 1e-4 px (positive sums, fp64 centre): a floor/ceil is certain unless
-    // the value lies within 1e-3 px of an integer (or anything looks degenerate) -> exact queue
-    const float e = 1e-3f;
+    // fp32 error of a bound (pixel units): the fp64 centre rounded to fp32 and the sums carry
+    // <= ~4 ulp of |bound| (2.4e-7 |f|); the half-width k sqrt(A) / px carries <= k dp sqrt(tr Sigma)
+    // / px with dp ~ 1.5e-6 the error of the fp32 projected axes (A = sum s p^2 with positive
+    // terms: Cauchy-Schwarz), bounded with sqrt(x) <= (x + 1) / 2.  A floor/ceil is certain unless
+    // the bound lies within e = 1e-4 + 2.4e-7 |f| + 5e-6 (tr Sigma / px^2 + 1) / 2 px of an integer
+    // (or anything looks degenerate) -> exact queue.  (e grows with D and with the Gaussian.)
+    const float trs = 2.5e-6f * fmaf(s3[0] + s3[1] + s3[2], ipxf * ipxf, 1.f);
+    auto nearint = [&](float f, float r) { return fabsf(f - r) < fmaf(2.4e-7f, fabsf(f), 1e-4f + trs); };
     // |bounds| < 2^21 keeps the magic-number rounding exact (the clip below goes to [-1, D])
     const bool okf = s3[0] >= 0.f && d2f > 0.f && fabsf(ampf) < 3e38f && fabsf(fu0) < 2e6f && fabsf(fu1) < 2e6f &&
                      fabsf(fv0) < 2e6f && fabsf(fv1) < 2e6f;
     const float ru0 = rint_fma(fu0), ru1 = rint_fma(fu1), rv0 = rint_fma(fv0), rv1 = rint_fma(fv1);
-    const bool near = fabsf(fu0 - ru0) < e || fabsf(fu1 - ru1) < e || fabsf(fv0 - rv0) < e || fabsf(fv1 - rv1) < e ||
+    const bool near = nearint(fu0, ru0) || nearint(fu1, ru1) || nearint(fv0, rv0) || nearint(fv1, rv1) ||
                       (tau > 0.0 && fabsf(fabsf(ampf) - tauf) <= 1e-4f * tauf);
     if (s3[0] >= 0.f && (!okf || near)) {   // deferred to the exact pass (compact, no warp divergence)
       queue[atomicAdd(&qn, 1)] = j;

@@ -826,3 +826,35 @@ def test_nonfinite_loss_is_reported(gem):
     with pytest.raises(b.GemError) as e:
         g["st"].stats()
     assert e.value.status == b.GEM_E_NONFINITE
+
+
+@pytest.mark.parametrize("D,tile", [(848, 8), (1696, 16)])
+def test_boxes_exact_at_large_D(gem, orc, D, tile):
+    """at large D one fp32 ulp of a pixel coordinate approaches the splat's exactness
+    margin; the margin now scales with |bound| (prep_bin.cu k_splat_count).  Gaussians spread over
+    the whole frame (|coordinates| up to ~D/2 px), one particle, the largest D each tile size
+    supports (the splat's shared tile histograms bound the tile grid; a larger D is rejected):
+    every AABB and list equals the oracle's (reading L22)."""
+    from paper_2509_25075_b200 import binding as b
+    with pytest.raises(b.GemError) as e:
+        gem.GemStep(gem.GemConfig(D=2 * D, pixel_size=0.5, n_gauss=10, max_batch=1, tile=tile))
+    assert e.value.status == b.GEM_E_INVALID
+    rng = np.random.default_rng(D)
+    N, px = 4000, 0.5
+    w = synth.Workload("big", N, D, px, 1)
+    mu = rng.uniform(-0.48, 0.48, (N, 3)) * D * px
+    ls = np.c_[np.log(rng.uniform(0.4, 6.0, (N, 3)) * px), np.zeros(N)]
+    q = rng.standard_normal((N, 4))
+    mr = np.c_[mu, rng.uniform(0.5, 1.5, N)]
+    rot, shift, ctf = synth.particles(w, 1, 7)
+    mr, ls, q, rot, shift, ctf = synth.f32(mr, ls, q, rot, shift, ctf)
+    obs = np.zeros((1, D, D), np.float32)
+    case = dict(w=w, params=(mr, ls, q), rot=rot, shift=shift, ctf=ctf, obs=obs, px=float(np.float32(px)))
+    st = gem.GemStep(gem.GemConfig(D=D, pixel_size=case["px"], n_gauss=N, max_batch=1, tile=tile))
+    P = gem.SoA.from_arrays(mr, ls, q, device=st.device)
+    t = lambda a: torch.from_numpy(a).to(st.device)
+    st.forward(P, t(rot), t(shift), t(ctf), t(obs))
+    torch.cuda.synchronize()
+    assert st.stats(check=False)["status"] == 0
+    ties = assert_lists_exact(orc, case, [st.export_lists(0)], tile)
+    assert ties == 0
