@@ -522,13 +522,17 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
   const unsigned lt = (1u << lane) - 1u;
   double w0 = 0.0, w1 = 0.0, w2 = 0.0;
   if (ZK) { w0 = (double)rot[9 * i + 2]; w1 = (double)rot[9 * i + 5]; w2 = (double)rot[9 * i + 8]; }
+  uint2 bnext = make_uint2(1u, 0u);   // the next step's box, loaded one step ahead
+  if (jsub + lane < c.N) bnext = boxi[jsub + lane];
   for (int step = 0; step < kSub / 32; ++step) {     // pass 2: deterministic fill
     const int j0 = jsub + step * 32;
     if (j0 >= c.N) break;
     const int j = j0 + lane;
+    const uint2 bcur = bnext;
+    if (step + 1 < kSub / 32 && j + 32 < c.N) bnext = boxi[j + 32];
     int tu0 = 0, tv0 = 0, ntu = 0, ntv = 0;
     if (j < c.N) {
-      const uint2 b = boxi[j];
+      const uint2 b = bcur;
       const int ulo = (int)(b.x & 0xffff), uhi = (int)(b.x >> 16), vlo = (int)(b.y & 0xffff), vhi = (int)(b.y >> 16);
       if (ulo <= uhi && vlo <= vhi) {
         tu0 = ulo >> c.tshift; tv0 = vlo >> c.tshift;
@@ -575,7 +579,37 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
     const int vy0 = __reduce_min_sync(0xffffffffu, act ? tv0 : 0x7fffffff);
     const int uw = (int)__reduce_max_sync(0xffffffffu, act ? (unsigned)(tu0 + ntu) : 0u) - ux0;
     const int uh = (int)__reduce_max_sync(0xffffffffu, act ? (unsigned)(tv0 + ntv) : 0u) - vy0;
-    if (uw * uh <= 64) {
+    if (uw * uh <= 64 && !__any_sync(0xffffffffu, ntu > 2 || ntv > 2)) {
+      // every rectangle within 2 x 2 tiles: the three phases unrolled over the four cells
+      unsigned *sm = smask + 64 * w;
+      const int cbase = (tv0 - vy0) * uw + (tu0 - ux0);
+      bool val[4];
+      int cell[4], tt[4], cur[4];
+      unsigned m[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int du = q & 1, dv = q >> 1;
+        val[q] = act && du < ntu && dv < ntv && kept(tu0 + du, tv0 + dv);
+        cell[q] = cbase + dv * uw + du;
+        tt[q] = (tv0 + dv) * c.nt + tu0 + du;
+        if (val[q]) atomicOr(&sm[cell[q]], 1u << lane);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (val[q]) { m[q] = sm[cell[q]]; cur[q] = mine[tt[q]]; }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (val[q]) {
+          put(cur[q] + __popc(m[q] & lt), j, key);
+          if (!(m[q] & lt)) {   // the tile's lowest lane advances the cursor and clears the word
+            mine[tt[q]] = cur[q] + __popc(m[q]);
+            sm[cell[q]] = 0u;
+          }
+        }
+      __syncwarp();
+    } else if (uw * uh <= 64) {
       unsigned *sm = smask + 64 * w;
       const int cbase = (tv0 - vy0) * uw + (tu0 - ux0);
       if (act)
