@@ -97,7 +97,6 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   const size_t Bm = (size_t)c.max_batch, W = (size_t)c.wave, N = (size_t)d.N, D = (size_t)d.D;
   const size_t H = D * (D / 2 + 1);
   L.n_hist = (int64_t)W * d.NT * d.C;
-  L.n_scan_blk = (L.n_hist + 4095) / 4096;
   L.list_cap = c.list_capacity;
   L.loss_blocks = ctf_loss_blocks(d.D);
   L.cufft_bytes = cufft_bytes;
@@ -106,10 +105,9 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.prep = take((sizeof(GaussPrep) + sizeof(GaussPrep32)) * N);   // fp64 prep, then fp32 prep
   L.rec = take(sizeof(SplatRec) * W * N);
   L.box = take(sizeof(uint2) * W * N);
-  L.hist = take(sizeof(int) * (size_t)L.n_hist);
+  L.hist = take(sizeof(int) * ((size_t)L.n_hist + W));   // [i][t][chunk] counts, then per-particle totals
   L.subcnt = take(sizeof(int) * (size_t)L.n_hist * 4);   // per fill-warp sub-chunk tile counts
   L.base = take(sizeof(int) * ((size_t)L.n_hist + 1));
-  L.scan_blk = take(sizeof(unsigned long long) * ((size_t)L.n_scan_blk + 1));   // scan look-back state
   L.ids = take(sizeof(int) * (size_t)L.list_cap);
   // + one zeroed row pair: the backward reads one pair below a box (render.cu k_render_bwd)
   L.proj = take(sizeof(float) * (W * D * D + 2 * D));
@@ -319,8 +317,6 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
   if (st != GEM_OK) { gem_destroy(ctx); return st; }
   if (cudaMemsetAsync(ctx->ws + L.stats, 0, sizeof(DevStats), ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(ctx->ws + L.ticket, 0, 64, ctx->stream) != cudaSuccess ||
-      cudaMemsetAsync(ctx->ws + L.scan_blk, 0, sizeof(unsigned long long) * ((size_t)L.n_scan_blk + 1), ctx->stream) !=
-          cudaSuccess ||
       cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
     gem_destroy(ctx);
     return GEM_E_CUDA;
@@ -454,14 +450,14 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     { Prof p(ctx, ctx->side, P_CTF_LOSS); launch_ctf_params(c, nb, ctf + 8 * (size_t)p0, ctx->ws + L.ctf_par, ctx->side, ctx->launches); CK(cudaGetLastError()); }
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
     const float *rw = rot + 9 * (size_t)p0;
-    { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist, at<int>(ctx, L.subcnt), st, s,
-                         ctx->launches); CK(cudaGetLastError()); }
     const int64_t nh = (int64_t)nb * c.NT * c.C;
+    int *ptot = hist + nh;   // per-particle entry totals (the splat adds, the scan reads)
+    CK(cudaMemsetAsync(ptot, 0, sizeof(int) * nb, s));
+    { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist, at<int>(ctx, L.subcnt), ptot, st, s,
+                         ctx->launches); CK(cudaGetLastError()); }
     {
       Prof p(ctx, s, P_SCAN);
-      launch_scan_1p(hist, base, nh, at<unsigned long long>(ctx, L.scan_blk), (nh + 4095) / 4096,
-                     ctx->scan_epoch = ctx->scan_epoch % 0x3ffffffeu + 1u,   // 1 .. 2^30 - 1 (state zeroed at init)
-                     at<int>(ctx, L.ticket) + 8, st, c.cap, s, ctx->launches);
+      launch_scan_pp(c, nb, hist, base, ptot, st, at<int>(ctx, L.ticket) + 8, s, ctx->launches);
       CK(cudaGetLastError());
     }
     uint2 *zpair = (c.flags & GEM_FLAG_ZSORT) ? at<uint2>(ctx, L.zs_key) : nullptr;

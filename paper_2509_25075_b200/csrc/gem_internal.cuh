@@ -38,10 +38,9 @@ struct __align__(16) SplatRec {
 };
 
 struct Layout {  // byte offsets into the caller's workspace
-  size_t prep, rec, box, hist, subcnt, base, scan_blk, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slots, acc, loss_part, ctf_par,
+  size_t prep, rec, box, hist, subcnt, base, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slots, acc, loss_part, ctf_par,
       stats, ticket, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, cufft_work2, zs_tmp, zs_key, zs_queue, total;
   int64_t n_hist;       // B_max * NT * C
-  int64_t n_scan_blk;
   int64_t list_cap;
   size_t cufft_bytes;
   int loss_blocks;      // CTF/loss partial blocks per particle
@@ -97,7 +96,6 @@ struct gem_ctx {
   int fused;           // GEM_FLAG_FUSED
   int last_p0, last_nb;  // the last wave of the last forward
   int launches;
-  unsigned scan_epoch;   // launch epoch of the single-pass scan's state words
   // profiling (gem_profile_enable): event pairs around launches
   int prof_on;
   int prof_n, prof_cap;
@@ -189,10 +187,10 @@ namespace gem {
 void launch_prep(const CfgDev &c, const float4 *mean_rho, const float4 *log_scale, const float4 *quat, GaussPrep *prep,
                  DevStats *st, cudaStream_t s, int &launches);
 void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
-                        const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, DevStats *st,
+                        const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, int *ptot, DevStats *st,
                         cudaStream_t s, int &launches);
-void launch_scan_1p(const int *in, int *out, int64_t n, unsigned long long *state, int64_t nblk, unsigned epoch,
-                    int *tk, DevStats *st, int64_t cap, cudaStream_t s, int &launches);
+void launch_scan_pp(const CfgDev &c, int B, const int *hist, int *base, const int *ptot, DevStats *st, int *tk,
+                    cudaStream_t s, int &launches);
 void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, DevStats *st, int64_t cap, cudaStream_t s,
                  int &launches);
 void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
                                                                const float *__restrict__ shift,
                                                                SplatRec *__restrict__ rec, uint2 *__restrict__ box,
                                                                int *__restrict__ hist, int *__restrict__ subcnt,
-                                                               DevStats *__restrict__ st) {
+                                                               int *__restrict__ ptot, DevStats *__restrict__ st) {
   // [kFillWarps][NT] tile histograms of the chunk's kFillWarps sub-chunks (one per k_fill warp),
   // then the exact-path queue [kChunk]
   extern __shared__ int shist[];
@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
   if ((tid & 31) == 0 && pairs) atomicAdd(&st->pairs, (unsigned long long)pairs);
   __syncthreads();
   int *sc = subcnt + ((size_t)i * c.C + ch) * kFillWarps * c.NT;
+  int ctot = 0;   // the chunk's entries, added to the particle's total (k_scan_pp's starts)
   for (int t = tid; t < c.NT; t += blockDim.x) {
     int tot = 0;
 #pragma unroll
@@ -318,7 +319,11 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
       tot += v;
     }
     hist[((size_t)i * c.NT + t) * c.C + ch] = tot;
+    ctot += tot;
   }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) ctot += __shfl_xor_sync(0xffffffffu, ctot, d);
+  if ((tid & 31) == 0 && ctot) atomicAdd(ptot + i, ctot);
 }
 
 // ------------------------------------------------------------------- scan
@@ -401,81 +406,48 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int *__restrict__ out
     if (base + k < n) out[base + k] += add;
 }
 
-// Single-pass exclusive scan (decoupled look-back): blocks take tiles in launch order from a
-// ticket, scan their tile, publish the tile aggregate, and thread 0 walks back over the
-// predecessors' published words (aggregate or inclusive prefix) until it meets an inclusive
-// prefix.  Words carry the launch epoch, so the state array needs no reset; the ticket resets
-// itself (last block out).  The last tile writes out[n] = total and the stats.
-constexpr int k1pThreads = 1024, k1pItems = 4, k1pTile = k1pThreads * k1pItems;
+// List offsets, one CTA per particle, with no inter-block dependency: the splat kernel added each
+// chunk's entry count to ptot[i], so CTA i starts its particle at pbase = sum_{i' < i} ptot[i']
+// (a block reduction) and writes pbase + the exclusive scan of its own [t][chunk] counts into
+// base[i][t][chunk] -- the global exclusive scan of the whole [i][t][chunk] array, in the layout
+// the fill, the render and the z-sort read (list (i, t) = ids[base[h] .. base[h + C]), h = (i NT +
+// t) C; the last CTA writes base[n] = all entries).  Entries beyond the capacity set the overflow
+// flags (the fill never writes past the buffer; the step's outputs are then invalid, include/gem.h).
+constexpr int kPpThreads = 1024;
 
-__global__ void __launch_bounds__(k1pThreads) k_scan_1p(const int *__restrict__ in, int *__restrict__ out, int64_t n,
-                                                          int64_t nblk, unsigned long long *state, unsigned epoch,
-                                                          int *tk, DevStats *st, int64_t cap) {
+__global__ void __launch_bounds__(kPpThreads) k_scan_pp(const int *__restrict__ hist, int *__restrict__ base, int seg,
+                                                        int B, const int *__restrict__ ptot, int64_t cap,
+                                                        DevStats *st, int *tk) {
   __shared__ int sw[33];
-  __shared__ int s_bid, s_prefix;
-  if (threadIdx.x == 0) s_bid = atomicAdd(tk, 1);
-  __syncthreads();
-  const int bid = s_bid;
-  const int64_t base = (int64_t)bid * k1pTile + (int64_t)threadIdx.x * k1pItems;
-  int v[k1pItems], s = 0;
+  const int i = blockIdx.x;
+  // this particle's start: the entries of the particles before it
+  int pb = 0;
+  for (int b = threadIdx.x; b < i; b += kPpThreads) pb += __ldg(ptot + b);
+  int pbase;
+  block_excl_scan(pb, sw, pbase);
+  const int *in = hist + (size_t)i * seg;
+  int *out = base + (size_t)i * seg;
+  // tiles of 4 kPpThreads items: each thread loads 4 consecutive counts (coalesced), one block
+  // scan per tile, the running total carried between tiles
+  int carry = pbase;
+  for (int t0 = 0; t0 < seg; t0 += 4 * kPpThreads) {
+    const int q = t0 + 4 * threadIdx.x;
+    int v[4];
 #pragma unroll
-  for (int k = 0; k < k1pItems; ++k) {
-    v[k] = (base + k < n) ? in[base + k] : 0;
-    s += v[k];
-  }
-  int total;
-  int e = block_excl_scan(s, sw, total);
-  const unsigned long long ep = (unsigned long long)(epoch & 0x3fffffffu) << 34;
-  volatile unsigned long long *vs = state;
-  if (threadIdx.x < 32) {   // warp 0: publish the aggregate, then look back 32 predecessors at a time
-    const int lane = threadIdx.x;
-    int prefix = 0;
-    if (bid > 0) {
-      if (lane == 0) {
-        vs[bid] = ep | (1ull << 32) | (unsigned)total;   // aggregate
-        __threadfence();
-      }
-      for (int j0 = bid - 1;;) {
-        const int j = j0 - lane;
-        unsigned long long w = 0;
-        bool ready = true;
-        if (j >= 0) {
-          w = vs[j];
-          ready = (w >> 34) == (ep >> 34);
-        }
-        if (!__all_sync(0xffffffffu, ready)) continue;        // some predecessor not published yet
-        const unsigned pmask = __ballot_sync(0xffffffffu, j >= 0 && ((w >> 32) & 3u) == 2u);
-        const int stop = pmask ? __ffs(pmask) - 1 : 31;       // nearest inclusive prefix in the window
-        int val = (j >= 0 && lane <= stop) ? (int)(unsigned)w : 0;
+    for (int k = 0; k < 4; ++k) v[k] = q + k < seg ? __ldg(in + q + k) : 0;
+    int total;
+    int run = block_excl_scan((v[0] + v[1]) + (v[2] + v[3]), sw, total);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        prefix += val;
-        if (pmask || j0 - 31 <= 0) break;
-        j0 -= 32;
-      }
+    for (int k = 0; k < 4; ++k) {
+      if (q + k < seg) out[q + k] = carry + run;
+      run += v[k];
     }
-    if (lane == 0) {
-      __threadfence();
-      vs[bid] = ep | (2ull << 32) | (unsigned)(prefix + total);   // inclusive prefix
-      s_prefix = prefix;
-    }
+    carry += total;
   }
-  __syncthreads();
-  e += s_prefix;
-#pragma unroll
-  for (int k = 0; k < k1pItems; ++k) {
-    if (base + k < n) out[base + k] = e;
-    e += v[k];
-  }
-  if (threadIdx.x == 0) {
-    if (bid == nblk - 1) {   // totals accumulate over the waves of one forward
-      const int tot = s_prefix + total;
-      out[n] = tot;
-      st->entries += (unsigned long long)tot;
-      if ((int64_t)tot > cap) { st->overflow = 1; tk[4] = 1; }   // tk[4]: sticky until gem_stats
-    }
-    __threadfence();
-    if (atomicAdd(tk + 1, 1) == (int)nblk - 1) { tk[0] = 0; tk[1] = 0; }
+  if (threadIdx.x == 0 && i == B - 1) {   // totals accumulate over the waves of one forward
+    base[(size_t)B * seg] = carry;
+    st->entries += (unsigned long long)carry;
+    if ((int64_t)carry > cap) { st->overflow = 1; tk[4] = 1; }   // tk[4]: sticky until gem_stats
   }
 }
 
@@ -702,7 +674,7 @@ void launch_prep(const CfgDev &c, const float4 *mean_rho, const float4 *log_scal
 }
 
 void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
-                        const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, DevStats *st,
+                        const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, int *ptot, DevStats *st,
                         cudaStream_t s, int &launches) {
   dim3 grid(c.C, B);
   const size_t smem = (kFillWarps * c.NT + kChunk) * sizeof(int);
@@ -713,9 +685,10 @@ void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const flo
     init = true;
   }
   if (c.flags & GEM_FLAG_EXACT_TILES)
-    k_splat_count<true><<<grid, kSplatThreads, smem, s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, subcnt, st);
+    k_splat_count<true><<<grid, kSplatThreads, smem, s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, subcnt, ptot, st);
   else
-    k_splat_count<false><<<grid, kSplatThreads, smem, s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, subcnt, st);
+    k_splat_count<false><<<grid, kSplatThreads, smem, s>>>(c, prep, mean_rho, rot, shift, rec, box, hist, subcnt, ptot,
+                                                           st);
   ++launches;
 }
 
@@ -727,11 +700,12 @@ void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, Dev
   launches += 3;
 }
 
-void launch_scan_1p(const int *in, int *out, int64_t n, unsigned long long *state, int64_t nblk, unsigned epoch,
-                    int *tk, DevStats *st, int64_t cap, cudaStream_t s, int &launches) {
-  k_scan_1p<<<(unsigned)nblk, k1pThreads, 0, s>>>(in, out, n, nblk, state, epoch, tk, st, cap);
+void launch_scan_pp(const CfgDev &c, int B, const int *hist, int *base, const int *ptot, DevStats *st, int *tk,
+                    cudaStream_t s, int &launches) {
+  k_scan_pp<<<B, kPpThreads, 0, s>>>(hist, base, c.NT * c.C, B, ptot, c.cap, st, tk);
   ++launches;
 }
+
 
 void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,
                  const float4 *mean_rho, const float *rot, uint2 *zpair, const SplatRec *rec, cudaStream_t s,
