@@ -858,3 +858,27 @@ def test_boxes_exact_at_large_D(gem, orc, D, tile):
     assert st.stats(check=False)["status"] == 0
     ties = assert_lists_exact(orc, case, [st.export_lists(0)], tile)
     assert ties == 0
+
+
+def test_render_volume_bitwise_reproducible(gem, orc):
+    """Row a11: brick lists are filled with atomics, but every brick sorts its list by Gaussian id
+    before accumulating (volume.cu k_vol_render), so repeated queries are bitwise identical; a
+    brick whose list exceeds the in-shared-memory sort (> 1024 entries: a dense cluster of wide
+    Gaussians) takes the global-memory ranking path, against the oracle too."""
+    case = make_case("T", B=1, seed=61, N=3000, D=32)
+    mr, ls, q = case["params"]
+    st = gem.GemStep(gem.GemConfig(D=32, pixel_size=4.0, n_gauss=3000, max_batch=1))
+    P = gem.SoA.from_arrays(mr, ls, q, device=st.device)
+    a = st.render_volume(P, 40, 4.0).cpu().numpy()
+    b = st.render_volume(P, 40, 4.0).cpu().numpy()
+    assert np.array_equal(a, b)
+    # 1500 wide Gaussians around the centre: >1024 entries in the central bricks
+    mr2, ls2 = mr.copy(), ls.copy()
+    mr2[:1500, :3] *= 0.05
+    ls2[:1500, :3] += 1.0
+    P2 = gem.SoA.from_arrays(mr2, ls2, q, device=st.device)
+    c = st.render_volume(P2, 40, 4.0).cpu().numpy()
+    d = st.render_volume(P2, 40, 4.0).cpu().numpy()
+    assert np.array_equal(c, d)
+    ref = orc.volume((mr2, ls2, q), 40, 4.0, masked=True)
+    assert maxnorm_rel(c, ref) < IMG_TOL
