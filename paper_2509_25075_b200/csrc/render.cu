@@ -266,6 +266,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
 // bitwise deterministic.  The row-pair recurrence squares V, so entries with |log2 V| > 60 at
 // an end row take the direct path too.
 constexpr int kLeWarps = 2, kLeBatch = 4;
+#ifndef GEM_FWD_L2PF
+#define GEM_FWD_L2PF 0
+#endif
 
 template <bool MK>
 __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, int B, const SplatRec *__restrict__ rec,
@@ -304,6 +307,16 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
     const int i = fdivmod(item, c.NT, c.inv_NT, t);
     const int tv = fdivmod(t, c.nt, c.inv_nt, tu);
     const int u0 = tu * T, v0 = tv * T;
+#if GEM_FWD_L2PF
+    // the warp that takes a particle's first tile has the records of the particle GEM_FWD_L2PF
+    // ahead prefetched into L2 by one bulk (TMA-engine) prefetch: the first gather of each
+    // record then hits L2 instead of HBM
+    if (t == 0 && lane == 0 && i + GEM_FWD_L2PF < B) {
+      const SplatRec *pf = rec + (size_t)(i + GEM_FWD_L2PF) * c.N;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"((unsigned)(c.N * sizeof(SplatRec)))
+                   : "memory");
+    }
+#endif
     if ((int64_t)e > c.cap) e = (int)c.cap;
     if ((int64_t)s > c.cap) s = (int)c.cap;
     float *out = proj + (size_t)i * c.D * c.D;
@@ -444,6 +457,9 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
 #ifndef GEM_BWD_UNROLL4
 #define GEM_BWD_UNROLL4 0
 #endif
+#ifndef GEM_BWD_TMA
+#define GEM_BWD_TMA 0
+#endif
 #ifndef GEM_BWD_MINB
 #define GEM_BWD_MINB 4
 #endif
@@ -461,6 +477,24 @@ __global__ void __launch_bounds__(kBwdBlock, GEM_BWD_MINB) k_render_bwd(CfgDev c
     const int p = threadIdx.x / 6, e = threadIdx.x % 6;
     sW[p][e] = rot[9 * (i0 + p) + 3 * (e % 3) + e / 3];   // W[row][col] = P[3 col + row], row = e / 3
   }
+#if GEM_BWD_TMA
+  // measured variant (not kept: 442.6 vs 433 us): each warp's 32 records of particle
+  // i0 + p (one contiguous 1 KB run) staged in shared memory by TMA bulk copies two particles
+  // ahead, per-warp double buffer and mbarriers
+  __shared__ __align__(128) SplatRec srec[kBwdBlock / 32][2][32];
+  __shared__ __align__(8) unsigned long long sbar[kBwdBlock / 32][2];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5, jw = blockIdx.x * blockDim.x + 32 * wq;
+  const unsigned tbytes = (unsigned)(max(min(32, c.N - jw), 0) * sizeof(SplatRec));
+  if (lane == 0 && tbytes) {
+    mbar_init(&sbar[wq][0], 1);
+    mbar_init(&sbar[wq][1], 1);
+    fence_mbar_init();
+    for (int p = 0; p < min(np, 2); ++p) {
+      mbar_expect_tx(&sbar[wq][p], tbytes);
+      tma_load_1d(srec[wq][p], rec + (size_t)(i0 + p) * c.N + jw, tbytes, &sbar[wq][p]);
+    }
+  }
+#endif
   __syncthreads();
   if (j >= c.N) return;
   __shared__ float sacc[10][kBwdBlock];   // the chunk's ten running sums (off the registers)
@@ -470,7 +504,17 @@ __global__ void __launch_bounds__(kBwdBlock, GEM_BWD_MINB) k_render_bwd(CfgDev c
 #pragma unroll 1
   for (int p = 0; p < np; ++p) {
   const int i = i0 + p;
+#if GEM_BWD_TMA
+  mbar_wait(&sbar[wq][p & 1], (p >> 1) & 1);
+  const SplatRec rr = srec[wq][p & 1][lane];
+  __syncwarp(__activemask());
+  if (lane == 0 && p + 2 < np) {
+    mbar_expect_tx(&sbar[wq][p & 1], tbytes);
+    tma_load_1d(srec[wq][p & 1], rec + (size_t)(i + 2) * c.N + jw, tbytes, &sbar[wq][p & 1]);
+  }
+#else
   const SplatRec rr = rec[(size_t)i * c.N + j];
+#endif
   const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
   const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
   if (ulo > uhi || vlo > vhi) continue;   // culled: contributes nothing
