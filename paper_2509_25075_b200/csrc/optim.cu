@@ -80,20 +80,38 @@ __global__ void __launch_bounds__(256) k_finalize(int N, int no_rot, const float
 
 // One batch (not fused): the backward's chunk sums [chunk][10][N] (render.cu k_render_bwd) are
 // added in chunk order and finalized in the same thread (no accumulator round trip).
-__global__ void __launch_bounds__(256) k_reduce_finalize(int nchunk, int N, int no_rot, const float *__restrict__ slots,
-                                                         const GaussPrep *__restrict__ prep,
-                                                         const float4 *__restrict__ mr, const float4 *__restrict__ ls,
-                                                         const float4 *__restrict__ q, float4 *__restrict__ g_mr,
-                                                         float4 *__restrict__ g_ls, float4 *__restrict__ g_q,
-                                                         DevStats *st) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= N) return;
-  float v[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int ch = 0; ch < nchunk; ++ch) {
-    const float *src = slots + (size_t)ch * 10 * N + j;
-#pragma unroll
-    for (int k = 0; k < 10; ++k) v[k] += __ldg(src + (size_t)k * N);
+// One block per 32 Gaussians: warp k sums component k of the 32 Gaussians over the chunks
+// (coalesced 128-byte rows, the chunks in order: the same fp32 sums as one thread per Gaussian),
+// then the first warp finalizes.  (One thread per Gaussian looping over all 10 x nchunk slots left
+// too few warps in flight: 196 blocks at N = 50 000.)
+constexpr int kRfG = 32;
+__global__ void __launch_bounds__(10 * kRfG) k_reduce_finalize(int nchunk, int N, int no_rot,
+                                                              const float *__restrict__ slots,
+                                                              const GaussPrep *__restrict__ prep,
+                                                              const float4 *__restrict__ mr,
+                                                              const float4 *__restrict__ ls,
+                                                              const float4 *__restrict__ q, float4 *__restrict__ g_mr,
+                                                              float4 *__restrict__ g_ls, float4 *__restrict__ g_q,
+                                                              DevStats *st) {
+  __shared__ float sv[10][kRfG];
+  const int jj = threadIdx.x % kRfG, k = threadIdx.x / kRfG, j = blockIdx.x * kRfG + jj;
+  float acc = 0.f;
+  if (j < N) {
+    const float *src = slots + (size_t)k * N + j;
+    int ch = 0;
+    for (; ch + 4 <= nchunk; ch += 4) {   // four loads in flight, added in chunk order
+      const float a0 = __ldg(src + (size_t)ch * 10 * N), a1 = __ldg(src + (size_t)(ch + 1) * 10 * N);
+      const float a2 = __ldg(src + (size_t)(ch + 2) * 10 * N), a3 = __ldg(src + (size_t)(ch + 3) * 10 * N);
+      acc += a0; acc += a1; acc += a2; acc += a3;
+    }
+    for (; ch < nchunk; ++ch) acc += __ldg(src + (size_t)ch * 10 * N);
   }
+  sv[k][jj] = acc;
+  __syncthreads();
+  if (k != 0 || j >= N) return;
+  float v[10];
+#pragma unroll
+  for (int m = 0; m < 10; ++m) v[m] = sv[m][jj];
   const float rho = mr[j].w;
   finalize_j(j, no_rot, make_float4(rho != 0.f ? v[0] / rho : 0.f, v[1], v[2], v[3]), make_float4(v[4], v[5], v[6], v[7]),
              make_float4(v[8], v[9], 0.f, 0.f), prep, mr, ls, q, g_mr, g_ls, g_q, st);
@@ -154,8 +172,9 @@ __global__ void __launch_bounds__(256) k_adam(int N, AdamArgs A) {
 void launch_reduce_finalize(const CfgDev &c, int B, const float *slots, const GaussPrep *prep, const float4 *mean_rho,
                             const float4 *log_scale, const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
                             int &launches) {
-  k_reduce_finalize<<<(c.N + 255) / 256, 256, 0, s>>>(bwd_chunks(B), c.N, c.flags & GEM_FLAG_NO_ROTATION ? 1 : 0, slots,
-                                                      prep, mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
+  k_reduce_finalize<<<(c.N + kRfG - 1) / kRfG, 10 * kRfG, 0, s>>>(bwd_chunks(B), c.N,
+                                                                  c.flags & GEM_FLAG_NO_ROTATION ? 1 : 0, slots, prep,
+                                                                  mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
   ++launches;
 }
 
