@@ -161,6 +161,9 @@ __device__ __noinline__ bool splat_exact(const GaussPrep &g, const double *W, do
 }
 
 constexpr int kSplatThreads = 256;
+#ifndef GEM_SPLAT_PF
+#define GEM_SPLAT_PF 1
+#endif
 constexpr int kFillWarps = 4, kSub = kChunk / kFillWarps;   // k_fill warps per chunk, Gaussians per warp
 
 template <bool PM>
@@ -234,11 +237,29 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
     rec[ij] = o;
     box[ij] = make_uint2((unsigned)(ulo & 0xffff) | ((unsigned)uhi << 16), (unsigned)(vlo & 0xffff) | ((unsigned)vhi << 16));
   };
+#if GEM_SPLAT_PF
+  // the next Gaussian's parameters are loaded one iteration ahead (L2 latency off the chain)
+  float4 m4n = make_float4(0.f, 0.f, 0.f, 0.f);
+  GaussPrep32 g32n;
+  {
+    const int j = ch * kChunk + tid;
+    if (j < c.N) { m4n = mr[j]; g32n = prep32[j]; }
+  }
+#endif
   for (int r = 0; r < kChunk / kSplatThreads; ++r) {
     const int j = ch * kChunk + r * kSplatThreads + tid;
     if (j >= c.N) break;
+#if GEM_SPLAT_PF
+    const float4 m4 = m4n;
+    const GaussPrep32 g32 = g32n;
+    if (r + 1 < kChunk / kSplatThreads && j + kSplatThreads < c.N) {
+      m4n = mr[j + kSplatThreads];
+      g32n = prep32[j + kSplatThreads];
+    }
+#else
     const float4 m4 = mr[j];
     const GaussPrep32 g32 = prep32[j];
+#endif
     // centre in fp64 (the record stores it relative to the box corner to ~1e-7 px)
     const double mx = fma(W[0], (double)m4.x, fma(W[1], (double)m4.y, fma(W[2], (double)m4.z, tx)));
     const double my = fma(W[3], (double)m4.x, fma(W[4], (double)m4.y, fma(W[5], (double)m4.z, ty)));
