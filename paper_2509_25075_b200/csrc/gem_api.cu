@@ -107,7 +107,8 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.box = take(sizeof(uint2) * W * N);
   L.hist = take(sizeof(int) * ((size_t)L.n_hist + W));   // [i][t][chunk] counts, then per-particle totals
   L.subcnt = take(sizeof(int) * (size_t)L.n_hist * 4);   // per fill-warp sub-chunk tile counts
-  L.base = take(sizeof(int) * ((size_t)L.n_hist + 1));
+  L.base = take(sizeof(int) * (size_t)L.n_hist);                  // [i][chunk][t] (the fill's cursors)
+  L.lst = take(sizeof(int) * ((size_t)W * d.NT + 1));              // list starts [i][t] + the total
   L.ids = take(sizeof(int) * (size_t)L.list_cap);
   // + one zeroed row pair: the backward reads one pair below a box (render.cu k_render_bwd)
   L.proj = take(sizeof(float) * (W * D * D + 2 * D));
@@ -457,19 +458,19 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
                          ctx->launches); CK(cudaGetLastError()); }
     {
       Prof p(ctx, s, P_SCAN);
-      launch_scan_pp(c, nb, hist, base, ptot, st, at<int>(ctx, L.ticket) + 8, s, ctx->launches);
+      launch_scan_pp(c, nb, hist, base, at<int>(ctx, L.lst), ptot, st, at<int>(ctx, L.ticket) + 8, s, ctx->launches);
       CK(cudaGetLastError());
     }
     uint2 *zpair = (c.flags & GEM_FLAG_ZSORT) ? at<uint2>(ctx, L.zs_key) : nullptr;
     { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<int>(ctx, L.subcnt), ids, (const float4 *)params->mean_rho, rw, zpair, rec, s, ctx->launches); CK(cudaGetLastError()); }
     if (zpair) {
       Prof p(ctx, s, P_ZSORT);
-      launch_zsort(c, nb, base, (const float4 *)params->mean_rho, rw, ids, zpair, at<int>(ctx, L.zs_tmp),
+      launch_zsort(c, nb, at<int>(ctx, L.lst), (const float4 *)params->mean_rho, rw, ids, zpair, at<int>(ctx, L.zs_tmp),
                    at<int>(ctx, L.zs_queue), s, ctx->launches);
       CK(cudaGetLastError());
     }
     float *proj = proj_out ? proj_out + p0 * DD : at<float>(ctx, L.proj);
-    { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, base, ids, proj, at<int>(ctx, L.ticket), s, ctx->launches); CK(cudaGetLastError()); }
+    { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, at<int>(ctx, L.lst), ids, proj, at<int>(ctx, L.ticket), s, ctx->launches); CK(cudaGetLastError()); }
     CKF(cufftSetStream(r2c, s));
     CKF(cufftSetStream(c2r, s));
     {
@@ -631,18 +632,18 @@ gem_status gem_export_lists(gem_ctx *ctx, int32_t particle, int32_t *tile_off, i
   CK(cudaStreamSynchronize(ctx->stream));
   const CfgDev &c = ctx->dc;
   const Layout &L = ctx->L;
-  const size_t seg = (size_t)c.NT * c.C;
-  int *hb = (int *)malloc(sizeof(int) * (seg + 1));
+  // list (particle, t) = ids[lst[particle NT + t] .. lst[particle NT + t + 1])
+  int *hb = (int *)malloc(sizeof(int) * (c.NT + 1));
   if (!hb) return GEM_E_INVALID;
-  if (cudaMemcpy(hb, at<int>(ctx, L.base) + (size_t)particle * seg, sizeof(int) * (seg + 1), cudaMemcpyDeviceToHost) !=
+  if (cudaMemcpy(hb, at<int>(ctx, L.lst) + (size_t)particle * c.NT, sizeof(int) * (c.NT + 1), cudaMemcpyDeviceToHost) !=
       cudaSuccess) {
     free(hb);
     return GEM_E_CUDA;
   }
   const int start = hb[0];
   if (tile_off)
-    for (int t = 0; t <= c.NT; ++t) tile_off[t] = hb[(size_t)t * c.C] - start;
-  const int64_t end = hb[seg];
+    for (int t = 0; t <= c.NT; ++t) tile_off[t] = hb[t] - start;
+  const int64_t end = hb[c.NT];
   free(hb);
   if (ids) {
     int64_t n = end - start;

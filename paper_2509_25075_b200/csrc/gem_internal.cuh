@@ -38,7 +38,7 @@ struct __align__(16) SplatRec {
 };
 
 struct Layout {  // byte offsets into the caller's workspace
-  size_t prep, rec, box, hist, subcnt, base, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slots, acc, loss_part, ctf_par,
+  size_t prep, rec, box, hist, subcnt, base, lst, ids, proj, spec_hat, spec_obs, spec_pred, dldi, slots, acc, loss_part, ctf_par,
       stats, ticket, stage_rot, stage_shift, stage_ctf, stage_obs, stage_loss, cufft_work, cufft_work2, zs_tmp, zs_key, zs_queue, total;
   int64_t n_hist;       // B_max * NT * C
   int64_t list_cap;
@@ -63,16 +63,21 @@ struct CfgDev {        // resolved config passed by value to kernels
   float inv_NT, inv_nt;             // 1 / NT, 1 / nt (fast exact division, see fdivmod)
 };
 
-// q = x / d, r = x % d for 0 <= x < 2^22 with a float reciprocal and an exact correction
+// q = x / d, r = x % d for 0 <= x < 2^22 with a float reciprocal and one branch-free correction
+// (x and d are exact in fp32 and inv = 1/d to 1 ulp, so the truncated estimate is off by at most 1)
 __device__ __forceinline__ int fdivmod(int x, int d, float inv, int &r) {
   int q = __float2int_rz((float)x * inv);
   r = x - q * d;
-  while (r < 0) { --q; r += d; }
-  while (r >= d) { ++q; r -= d; }
+  q += (r >= d) - (r < 0);
+  r = x - q * d;
   return q;
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// List offsets (a3): base[(i C + chunk) NT + t] = start of chunk's entries in list (i, t) (the
+// fill's cursors), and lst[i NT + t] = start of list (i, t), lst[B NT] = all entries: list (i, t)
+// spans ids[lst[it] .. lst[it + 1]), it = i NT + t (the render, z-sort and export read lst).
 
 }  // namespace gem
 
@@ -189,8 +194,8 @@ void launch_prep(const CfgDev &c, const float4 *mean_rho, const float4 *log_scal
 void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
                         const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, int *ptot, DevStats *st,
                         cudaStream_t s, int &launches);
-void launch_scan_pp(const CfgDev &c, int B, const int *hist, int *base, const int *ptot, DevStats *st, int *tk,
-                    cudaStream_t s, int &launches);
+void launch_scan_pp(const CfgDev &c, int B, const int *hist, int *base, int *lst, const int *ptot, DevStats *st,
+                    int *tk, cudaStream_t s, int &launches);
 void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, DevStats *st, int64_t cap, cudaStream_t s,
                  int &launches);
 void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,

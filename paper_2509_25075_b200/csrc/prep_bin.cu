@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
       sc[w * c.NT + t] = v;
       tot += v;
     }
-    hist[((size_t)i * c.NT + t) * c.C + ch] = tot;
+    hist[((size_t)i * c.C + ch) * c.NT + t] = tot;   // [i][chunk][t]: coalesced
     ctot += tot;
   }
 #pragma unroll
@@ -429,18 +429,19 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int *__restrict__ out
 
 // List offsets, one CTA per particle, with no inter-block dependency: the splat kernel added each
 // chunk's entry count to ptot[i], so CTA i starts its particle at pbase = sum_{i' < i} ptot[i']
-// (a block reduction) and writes pbase + the exclusive scan of its own [t][chunk] counts into
-// base[i][t][chunk] -- the global exclusive scan of the whole [i][t][chunk] array, in the layout
-// the fill, the render and the z-sort read (list (i, t) = ids[base[h] .. base[h + C]), h = (i NT +
-// t) C; the last CTA writes base[n] = all entries).  Entries beyond the capacity set the overflow
+// (a block reduction) and writes pbase + the exclusive scan, in (tile, chunk) order, of its own
+// counts: the global exclusive scan of the whole array in (i, t, chunk) order, stored in the
+// [i][chunk][t] layout the splat writes and the fill reads coalesced (list_bounds for the
+// readers) plus each list's start in lst[i NT + t] (the last CTA writes lst[B NT] = all entries).  Entries beyond the capacity set the overflow
 // flags (the fill never writes past the buffer; the step's outputs are then invalid, include/gem.h).
 constexpr int kPpThreads = 1024;
 
-__global__ void __launch_bounds__(kPpThreads) k_scan_pp(const int *__restrict__ hist, int *__restrict__ base, int seg,
-                                                        int B, const int *__restrict__ ptot, int64_t cap,
-                                                        DevStats *st, int *tk) {
+__global__ void __launch_bounds__(kPpThreads) k_scan_pp(const int *__restrict__ hist, int *__restrict__ base,
+                                                        int *__restrict__ lst, int NT, int C, int B,
+                                                        const int *__restrict__ ptot, int64_t cap, DevStats *st,
+                                                        int *tk) {
   __shared__ int sw[33];
-  const int i = blockIdx.x;
+  const int i = blockIdx.x, seg = NT * C;
   // this particle's start: the entries of the particles before it
   int pb = 0;
   for (int b = threadIdx.x; b < i; b += kPpThreads) pb += __ldg(ptot + b);
@@ -448,25 +449,35 @@ __global__ void __launch_bounds__(kPpThreads) k_scan_pp(const int *__restrict__ 
   block_excl_scan(pb, sw, pbase);
   const int *in = hist + (size_t)i * seg;
   int *out = base + (size_t)i * seg;
-  // tiles of 4 kPpThreads items: each thread loads 4 consecutive counts (coalesced), one block
-  // scan per tile, the running total carried between tiles
+  // scan order (t, chunk) over the [chunk][t] layout (the particle's 4 NT C bytes sit in L1):
+  // tiles of 4 kPpThreads items, 4 consecutive (t, chunk) items per thread, the running total
+  // carried between tiles
   int carry = pbase;
-  for (int t0 = 0; t0 < seg; t0 += 4 * kPpThreads) {
-    const int q = t0 + 4 * threadIdx.x;
-    int v[4];
+  for (int f0 = 0; f0 < seg; f0 += 4 * kPpThreads) {
+    const int f = f0 + 4 * threadIdx.x;
+    int v[4], idx[4], tl[4];
+    int t = f / C, ch = f - t * C;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = q + k < seg ? __ldg(in + q + k) : 0;
+    for (int k = 0; k < 4; ++k) {
+      idx[k] = ch * NT + t;
+      tl[k] = ch == 0 ? t : -1;   // the list's own start (chunk 0)
+      v[k] = f + k < seg ? __ldg(in + idx[k]) : 0;
+      if (++ch == C) { ch = 0; ++t; }
+    }
     int total;
     int run = block_excl_scan((v[0] + v[1]) + (v[2] + v[3]), sw, total);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (q + k < seg) out[q + k] = carry + run;
+      if (f + k < seg) {
+        out[idx[k]] = carry + run;
+        if (tl[k] >= 0) lst[(size_t)i * NT + tl[k]] = carry + run;
+      }
       run += v[k];
     }
     carry += total;
   }
   if (threadIdx.x == 0 && i == B - 1) {   // totals accumulate over the waves of one forward
-    base[(size_t)B * seg] = carry;
+    lst[(size_t)B * NT] = carry;
     st->entries += (unsigned long long)carry;
     if ((int64_t)carry > cap) { st->overflow = 1; tk[4] = 1; }   // tk[4]: sticky until gem_stats
   }
@@ -503,7 +514,7 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
   // splat kernel counted each sub-chunk's entries per tile)
   const int *sc = subcnt + ((size_t)i * c.C + ch) * kFillWarps * c.NT;
   for (int t = threadIdx.x; t < c.NT; t += blockDim.x) {
-    int run = base[((size_t)i * c.NT + t) * c.C + ch];
+    int run = base[((size_t)i * c.C + ch) * c.NT + t];
 #pragma unroll
     for (int ww = 0; ww < kFillWarps; ++ww) {
       cnt[ww * c.NT + t] = run;
@@ -721,9 +732,9 @@ void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, Dev
   launches += 3;
 }
 
-void launch_scan_pp(const CfgDev &c, int B, const int *hist, int *base, const int *ptot, DevStats *st, int *tk,
-                    cudaStream_t s, int &launches) {
-  k_scan_pp<<<B, kPpThreads, 0, s>>>(hist, base, c.NT * c.C, B, ptot, c.cap, st, tk);
+void launch_scan_pp(const CfgDev &c, int B, const int *hist, int *base, int *lst, const int *ptot, DevStats *st,
+                    int *tk, cudaStream_t s, int &launches) {
+  k_scan_pp<<<B, kPpThreads, 0, s>>>(hist, base, lst, c.NT, c.C, B, ptot, c.cap, st, tk);
   ++launches;
 }
 

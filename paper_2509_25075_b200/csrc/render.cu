@@ -105,10 +105,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
   auto bounds = [&](int it, int &s_, int &e_) {
     s_ = 0; e_ = 0;
     if (it < items) {
-      const int ii = it / c.NT, tt = it - ii * c.NT;
-      const size_t h = ((size_t)ii * c.NT + tt) * c.C;
-      s_ = base[h];
-      e_ = base[h + c.C];
+      s_ = base[it];   // base = lst here (list starts, see list_bounds' comment)
+      e_ = base[it + 1];
     }
   };
   int nitem = next_item(ticket, lane), ns, ne;
@@ -285,9 +283,8 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
   auto bounds = [&](int it, int &s_, int &e_) {
     s_ = 0; e_ = 0;
     if (it < items) {
-      const size_t h = (size_t)it * c.C;   // it = i * NT + t
-      s_ = base[h];
-      e_ = base[h + c.C];
+      s_ = base[it];   // base = lst here: list (i, t) = ids[lst[it] .. lst[it + 1]), it = i NT + t
+      e_ = base[it + 1];
     }
   };
   int bat = kLeBatch * next_item(ticket, lane), pos = 0;

@@ -65,9 +65,8 @@ __device__ __forceinline__ bool kless(unsigned ka, int ja, unsigned kb, int jb) 
 }
 
 __device__ __forceinline__ void segment(const CfgDev &c, const int *__restrict__ base, int g, int64_t &s, int &n) {
-  const size_t h = (size_t)g * c.C;   // g = i * NT + t
-  s = base[h];
-  int64_t e = base[h + c.C];
+  s = base[g];   // base = lst: list (i, t) = ids[lst[g] .. lst[g + 1]), g = i * NT + t
+  int64_t e = base[g + 1];
   if (e > c.cap) e = c.cap;
   n = (int)(e - s);
 }
