@@ -161,6 +161,9 @@ __device__ __noinline__ bool splat_exact(const GaussPrep &g, const double *W, do
 }
 
 constexpr int kSplatThreads = 256;
+#ifndef GEM_FILL_BOXCS
+#define GEM_FILL_BOXCS 0
+#endif
 #ifndef GEM_SPLAT_PF
 #define GEM_SPLAT_PF 1
 #endif
@@ -527,13 +530,18 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
   double w0 = 0.0, w1 = 0.0, w2 = 0.0;
   if (ZK) { w0 = (double)rot[9 * i + 2]; w1 = (double)rot[9 * i + 5]; w2 = (double)rot[9 * i + 8]; }
   uint2 bnext = make_uint2(1u, 0u);   // the next step's box, loaded one step ahead
-  if (jsub + lane < c.N) bnext = boxi[jsub + lane];
+#if GEM_FILL_BOXCS   // the boxes are read once: evict-first
+#define LDBOX(p_) __ldcs(p_)
+#else
+#define LDBOX(p_) (*(p_))
+#endif
+  if (jsub + lane < c.N) bnext = LDBOX(boxi + jsub + lane);
   for (int step = 0; step < kSub / 32; ++step) {     // pass 2: deterministic fill
     const int j0 = jsub + step * 32;
     if (j0 >= c.N) break;
     const int j = j0 + lane;
     const uint2 bcur = bnext;
-    if (step + 1 < kSub / 32 && j + 32 < c.N) bnext = boxi[j + 32];
+    if (step + 1 < kSub / 32 && j + 32 < c.N) bnext = LDBOX(boxi + j + 32);
     int tu0 = 0, tv0 = 0, ntu = 0, ntv = 0;
     if (j < c.N) {
       const uint2 b = bcur;

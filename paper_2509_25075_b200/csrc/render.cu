@@ -9,6 +9,15 @@
 // Both use multiplicative recurrences instead of one exp per pixel (see the forward's comment).
 #include "gem_internal.cuh"
 
+#ifndef GEM_FWD_IDCS
+#define GEM_FWD_IDCS 0
+#endif
+#if GEM_FWD_IDCS   // the tile lists' ids stream through once: evict-first loads
+#define LDID(p_) __ldcs(p_)
+#else
+#define LDID(p_) (*(p_))
+#endif
+
 namespace gem {
 namespace {
 
@@ -144,7 +153,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
       const int q = g0 + lane, qc = g0 % kCH + lane;   // list position, index within the chunk
       const SplatRec rr = nxt;
       if (q + 32 < nall) nxt = reci[id2];
-      if (q + 64 < nall) id2 = ids[s + q + 64];
+      if (q + 64 < nall) id2 = LDID(ids + s + q + 64);
       int pr0 = NP, pr1 = -1;
       if (q < nall) {
         const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
@@ -331,14 +340,14 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
       for (int k = 0; k < T; ++k) acc[p][k] = make_float2(0.f, 0.f);
     const SplatRec *reci = rec + (size_t)i * c.N;
     const int nall = e - s;
-    int id2 = 32 + lane < nall ? ids[s + 32 + lane] : 0;
+    int id2 = 32 + lane < nall ? LDID(ids + s + 32 + lane) : 0;
     SplatRec nxt;
-    if (lane < nall) nxt = reci[ids[s + lane]];
+    if (lane < nall) nxt = reci[LDID(ids + s + lane)];
     for (int g0 = 0; g0 < nall; g0 += 32) {
       const int q = g0 + lane;
       const SplatRec rr = nxt;
       if (q + 32 < nall) nxt = reci[id2];
-      if (q + 64 < nall) id2 = ids[s + q + 64];
+      if (q + 64 < nall) id2 = LDID(ids + s + q + 64);
       if (q >= nall) continue;
       const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
       const int ulo = (ub & 0xffff) - u0, uhi = (ub >> 16) - u0, vlo = (vb & 0xffff) - v0, vhi = (vb >> 16) - v0;
@@ -454,6 +463,9 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
 #ifndef GEM_BWD_UNROLL4
 #define GEM_BWD_UNROLL4 0
 #endif
+#ifndef GEM_BWD_CS
+#define GEM_BWD_CS 1
+#endif
 #ifndef GEM_BWD_TMA
 #define GEM_BWD_TMA 0
 #endif
@@ -510,7 +522,14 @@ __global__ void __launch_bounds__(kBwdBlock, GEM_BWD_MINB) k_render_bwd(CfgDev c
     tma_load_1d(srec[wq][p & 1], rec + (size_t)(i + 2) * c.N + jw, tbytes, &sbar[wq][p & 1]);
   }
 #else
+#if GEM_BWD_CS
+  // the records stream through once: evict-first (.cs), so that they do not push dL/dI out of L2
+  SplatRec rr;
+  rr.f0 = __ldcs(&rec[(size_t)i * c.N + j].f0);
+  rr.f1 = __ldcs(&rec[(size_t)i * c.N + j].f1);
+#else
   const SplatRec rr = rec[(size_t)i * c.N + j];
+#endif
 #endif
   const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
   const int ulo = ub & 0xffff, uhi = ub >> 16, vlo = vb & 0xffff, vhi = vb >> 16;
