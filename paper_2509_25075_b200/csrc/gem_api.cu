@@ -318,6 +318,12 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
   if (st != GEM_OK) { gem_destroy(ctx); return st; }
   if (cudaMemsetAsync(ctx->ws + L.stats, 0, sizeof(DevStats), ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(ctx->ws + L.ticket, 0, 64, ctx->stream) != cudaSuccess ||
+      // the backward reads one row pair below a box: the image buffers (and their pad pair) start
+      // zeroed, so that read is finite even past the batch's last image
+      cudaMemsetAsync(ctx->ws + L.proj, 0, sizeof(float) * ((size_t)c.wave * c.D * c.D + 2 * c.D), ctx->stream) !=
+          cudaSuccess ||
+      cudaMemsetAsync(ctx->ws + L.dldi, 0, sizeof(float) * ((size_t)c.wave * c.D * c.D + 2 * c.D), ctx->stream) !=
+          cudaSuccess ||
       cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
     gem_destroy(ctx);
     return GEM_E_CUDA;

@@ -579,8 +579,9 @@ __global__ void __launch_bounds__(kBwdBlock, GEM_BWD_MINB) k_render_bwd(CfgDev c
   if (!slow) {
     // two row pairs per iteration (independent chains: twice the loads in flight); rows outside
     // the box carry E = 0.  The second pair is always read one pair below the first (a constant
-    // offset); when it lies wholly below the box its update is predicated off (its memory is
-    // valid: the next image's rows, or the buffer's one-pair pad after the last image)
+    // offset): when it lies wholly below the box it reads the next image's first rows, or the
+    // buffer's zeroed one-pair pad after the last image -- finite values times E = 0 (a
+    // non-finite dL/dI anywhere already makes the step non-finite, GEM_E_NONFINITE)
     auto adv = [&]() { El *= V; V *= W; Rl *= Kb; };
 #pragma unroll 1
     for (int r = -(vlo & 1); r < ht; r += 4) {
@@ -597,7 +598,7 @@ __global__ void __launch_bounds__(kBwdBlock, GEM_BWD_MINB) k_render_bwd(CfgDev c
         const float2 Ea = MK ? make_float2(E0.x >= ethr ? E0.x : 0.f, E0.y >= ethr ? E0.y : 0.f) : E0;
         const float2 Eb = MK ? make_float2(E1.x >= ethr ? E1.x : 0.f, E1.y >= ethr ? E1.y : 0.f) : E1;
         C0 = __ffma2_rn(ga, Ea, C0);   // C += h, h = g e
-        if (a1) C1 = __ffma2_rn(gb, Eb, C1);
+        C1 = __ffma2_rn(gb, Eb, C1);   // Eb = 0 below the box: the read pair is finite (pad zeroed)
         Q0 = __fadd2_rn(Q0, C0);
         Q1 = __fadd2_rn(Q1, C1);
         Z0 = __fadd2_rn(Z0, Q0);
