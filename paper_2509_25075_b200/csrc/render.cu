@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(CfgDev c, int B, 
 // shuffles (halving 64 -> 2 values per lane; lane L ends with row pair L / 8, column L % 8):
 // bitwise deterministic.  The row-pair recurrence squares V, so entries with |log2 V| > 60 at
 // an end row take the direct path too.
-constexpr int kLeWarps = 2, kLeBatch = 4;
+constexpr int kLeWarps = 2, kLeBatch = 4, kLePitch = 68;   // kLePitch: the reduction buffer's row pitch
 #ifndef GEM_FWD_L2PF
 #define GEM_FWD_L2PF 0
 #endif
@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
                                                                     float *__restrict__ proj, int *ticket) {
   constexpr int T = 8;
   constexpr float nh = -0.5f * kLog2e;
+  __shared__ __align__(16) float le_smem[kLeWarps * 32 * kLePitch];
   const float eK = MK ? ex2(nh * c.k * c.k) : 0.f;
   const int lane = threadIdx.x & 31;
   const int items = B * c.NT;
@@ -421,25 +422,26 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
         }
       }
     }
-    // reduce-scatter of the 32 private tiles: flattened index n = 16 p + 2 k + (0: .x, 1: .y);
-    // after halving on lane bits 16, 8, 4, 2, 1 lane L holds n = 2L, 2L + 1
-    float v[64];
+    // sum of the 32 private tiles (flattened index n = 16 p + 2 k + (0: .x, 1: .y)) through the
+    // warp's shared buffer: lane L stores its copy as row L (16 x 128-bit stores; row pitch 68
+    // floats: 4-way, i.e. conflict-free, 128-bit stores), then sums column pair (2L, 2L + 1) over
+    // the 32 rows in lane order (32 x 64-bit loads, conflict-free): lane L ends with row pair L / 8,
+    // column L % 8.  Fixed order: bitwise deterministic.
+    float *buf = le_smem + (threadIdx.x >> 5) * (32 * kLePitch);
+    __syncwarp();   // the previous item's reads are done
 #pragma unroll
     for (int p = 0; p < 4; ++p)
 #pragma unroll
-      for (int k = 0; k < T; ++k) { v[16 * p + 2 * k] = acc[p][k].x; v[16 * p + 2 * k + 1] = acc[p][k].y; }
+      for (int k = 0; k < T; k += 2)
+        *reinterpret_cast<float4 *>(buf + lane * kLePitch + 16 * p + 2 * k) =
+            make_float4(acc[p][k].x, acc[p][k].y, acc[p][k + 1].x, acc[p][k + 1].y);
+    __syncwarp();
+    float2 sum = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int o = 16, h = 32; o >= 1; o >>= 1, h >>= 1) {
-      const bool up = (lane & o) != 0;
-#pragma unroll
-      for (int n = 0; n < h; ++n) {
-        const float keep = up ? v[n + h] : v[n], send = up ? v[n] : v[n + h];
-        v[n] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-    }
+    for (int r = 0; r < 32; ++r) sum = __fadd2_rn(sum, *reinterpret_cast<const float2 *>(buf + r * kLePitch + 2 * lane));
     const int u = u0 + (lane & 7), vr = v0 + 2 * (lane >> 3);
-    if (u < c.D && vr < c.D) out[(size_t)vr * c.D + u] = v[0];
-    if (u < c.D && vr + 1 < c.D) out[(size_t)(vr + 1) * c.D + u] = v[1];
+    if (u < c.D && vr < c.D) out[(size_t)vr * c.D + u] = sum.x;
+    if (u < c.D && vr + 1 < c.D) out[(size_t)(vr + 1) * c.D + u] = sum.y;
   }
   retire(ticket, lane);
 }
@@ -462,6 +464,9 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
 // instead of 6 per (i, j).
 #ifndef GEM_BWD_UNROLL4
 #define GEM_BWD_UNROLL4 0
+#endif
+#ifndef GEM_BWD_RPF
+#define GEM_BWD_RPF 0
 #endif
 #ifndef GEM_BWD_CS
 #define GEM_BWD_CS 1
@@ -510,6 +515,11 @@ __global__ void __launch_bounds__(kBwdBlock, GEM_BWD_MINB) k_render_bwd(CfgDev c
   float *vacc = &sacc[0][threadIdx.x];     // vacc[k * kBwdBlock] = sum k
 #pragma unroll
   for (int k = 0; k < 10; ++k) vacc[k * kBwdBlock] = 0.f;
+#if GEM_BWD_RPF
+  SplatRec rnext;
+  rnext.f0 = __ldcs(&rec[(size_t)i0 * c.N + j].f0);
+  rnext.f1 = __ldcs(&rec[(size_t)i0 * c.N + j].f1);
+#endif
 #pragma unroll 1
   for (int p = 0; p < np; ++p) {
   const int i = i0 + p;
@@ -522,7 +532,14 @@ __global__ void __launch_bounds__(kBwdBlock, GEM_BWD_MINB) k_render_bwd(CfgDev c
     tma_load_1d(srec[wq][p & 1], rec + (size_t)(i + 2) * c.N + jw, tbytes, &sbar[wq][p & 1]);
   }
 #else
-#if GEM_BWD_CS
+#if GEM_BWD_RPF
+  // the next particle's record loaded one iteration ahead (registers), evict-first
+  const SplatRec rr = rnext;
+  if (p + 1 < np) {
+    rnext.f0 = __ldcs(&rec[(size_t)(i + 1) * c.N + j].f0);
+    rnext.f1 = __ldcs(&rec[(size_t)(i + 1) * c.N + j].f1);
+  }
+#elif GEM_BWD_CS
   // the records stream through once: evict-first (.cs), so that they do not push dL/dI out of L2
   SplatRec rr;
   rr.f0 = __ldcs(&rec[(size_t)i * c.N + j].f0);
