@@ -341,6 +341,19 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
       for (int k = 0; k < T; ++k) acc[p][k] = make_float2(0.f, 0.f);
     const SplatRec *reci = rec + (size_t)i * c.N;
     const int nall = e - s;
+#if GEM_FWD_DPF
+    // records two rounds ahead, ids three
+    int id3 = 64 + lane < nall ? LDID(ids + s + 64 + lane) : 0;
+    SplatRec nxt, nxt2;
+    if (lane < nall) nxt = reci[LDID(ids + s + lane)];
+    if (32 + lane < nall) nxt2 = reci[LDID(ids + s + 32 + lane)];
+    for (int g0 = 0; g0 < nall; g0 += 32) {
+      const int q = g0 + lane;
+      const SplatRec rr = nxt;
+      nxt = nxt2;
+      if (q + 64 < nall) nxt2 = reci[id3];
+      if (q + 96 < nall) id3 = LDID(ids + s + q + 96);
+#else
     int id2 = 32 + lane < nall ? LDID(ids + s + 32 + lane) : 0;
     SplatRec nxt;
     if (lane < nall) nxt = reci[LDID(ids + s + lane)];
@@ -349,6 +362,7 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
       const SplatRec rr = nxt;
       if (q + 32 < nall) nxt = reci[id2];
       if (q + 64 < nall) id2 = LDID(ids + s + q + 64);
+#endif
       if (q >= nall) continue;
       const int ub = __float_as_int(rr.f1.z), vb = __float_as_int(rr.f1.w);
       const int ulo = (ub & 0xffff) - u0, uhi = (ub >> 16) - u0, vlo = (vb & 0xffff) - v0, vhi = (vb >> 16) - v0;
