@@ -3,7 +3,7 @@
 # ncu launch list of the bench command, --set full captures of the step's main kernels and of the
 # measured TMA variants.  Everything under gpurun_out/round2/ (summaries copied to profiles/r2/).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-TAG=${TAG:-r2}
+TAG=${TAG:-r2b}
 O=gpurun_out/round2
 mkdir -p $O
 nvidia-smi > $O/nvidia-smi.txt 2>&1
@@ -33,4 +33,8 @@ for v in "-DGEM_BWD_TMA=1:k_render_bwd:bwd_tma" "-DGEM_FWD_L2PF=2:k_render_fwd:f
   python tools/ncu_stalls.py $O/full_$name.ncu-rep >> $O/ncu_full_summary_$name.txt 2>&1
 done
 python -c "from paper_2509_25075_b200 import build as b; b.build(force=True)" > /dev/null 2>&1
+# other workloads and batch sizes (no cpu baseline / e2e): S, P and the batch sweep at R
+for a in "--config S" "--config P" "--batch 128" "--batch 512" "--state init"; do
+  timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-volume $a > "$O/bench_$(echo $a | tr -d ' -')_$TAG.json" 2>/dev/null
+done
 tail -2 $O/pytest_gpu.log; tail -2 $O/smoke.log; tail -1 $O/bench_$TAG.err
