@@ -510,9 +510,9 @@ def main():
         hbm = float(peaks.get("hbm_gbs", 6537.6))
         vol = {"Dv": Dv, "voxel_A": px, "ms": vms, "ms_per_call_with_host_sync": ve0.elapsed_time(ve1) / 5,
                "achieved_gbs": 4.0 * Dv ** 3 / (vms * 1e-3) / 1e9, "peak_gbs": hbm,
-               "frac": 4.0 * Dv ** 3 / (vms * 1e-3) / 1e9 / hbm, "bound": "issue (the per-hit brick loop); frac is against the HBM floor of the 4 Dv^3 B write",
+               "frac": 4.0 * Dv ** 3 / (vms * 1e-3) / 1e9 / hbm, "bound": "latency (the per-sub-brick record chain) + XU; frac is against the HBM floor of the 4 Dv^3 B write",
                "gpu_launches_per_call": (sc.launches - l0) / 5,
-               "includes": "brick count, scan, brick-list fill and the per-brick render; the call's overflow "
+               "includes": "brick count, scan, brick-list fill, staging (sorted brick-local records, empty bricks zeroed) and the sub-brick render; the call's overflow "
                            "check (a 24 B D2H + stream sync) only in ms_per_call_with_host_sync"}
         del vout
 

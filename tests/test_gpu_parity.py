@@ -256,6 +256,38 @@ def test_render_volume_bricks(gem, orc, stretch):
         assert maxnorm_rel(vol, ref) < IMG_TOL, Dv
 
 
+def test_render_volume_full_grid(gem, orc):
+    """Row a11 at the bench's grid: Dv = D = 256 of config R (32^3 bricks, the headline model's
+    Gaussian sizes), on a seeded 1200-Gaussian subset of the steady model so the fp64 oracle
+    finishes in seconds; the whole 256^3 volume is compared."""
+    w = synth.CONFIGS["R"]
+    mr, ls, q = synth.f32(*synth.steady_model(w, 0))
+    sel = np.sort(np.random.default_rng(5).choice(w.N, 1200, replace=False))
+    mr, ls, q = mr[sel], ls[sel], q[sel]
+    vs = float(np.float32(w.px))
+    st = gem.GemStep(gem.GemConfig(D=w.D, pixel_size=vs, n_gauss=len(sel), max_batch=1))
+    P = gem.SoA.from_arrays(mr, ls, q, device=st.device)
+    vol = st.render_volume(P, w.D, vs).cpu().numpy()
+    ref = orc.volume((mr, ls, q), w.D, vs, masked=True)
+    assert maxnorm_rel(vol, ref) < IMG_TOL
+
+
+def test_render_volume_large_grid(gem, orc):
+    """Dv = 416 (> 2^17 bricks): the general multi-block scan, every brick's slot taken by the
+    fill's atomic (no pre-taken slots), against the oracle."""
+    case = make_case("T", B=1, seed=71, N=80, D=32)
+    mr, ls, q = case["params"]
+    mr = mr.copy()
+    mr[:, :3] *= 6.0   # spread over the large grid
+    vs = 2.0
+    st = gem.GemStep(gem.GemConfig(D=32, pixel_size=vs, n_gauss=80, max_batch=1))
+    P = gem.SoA.from_arrays(mr, ls, q, device=st.device)
+    vol = st.render_volume(P, 416, vs).cpu().numpy()
+    ref = orc.volume((mr, ls, q), 416, vs, masked=True)
+    assert np.abs(ref).max() > 0
+    assert maxnorm_rel(vol, ref) < IMG_TOL
+
+
 def test_empty_lists_all_offframe(gem):
     case = make_case("T", B=2, seed=9)
     mr = case["params"][0].copy()
