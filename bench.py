@@ -369,9 +369,10 @@ def main():
 
     # ---- e2e: the same steps from pinned HOST inputs through the C ABI's own host path
     # (gem_batch.memory = GEM_MEM_HOST: every call copies its poses, CTFs and observed images
-    # host->device -- the images on libgem's side stream, overlapped with the splat / binning /
-    # render -- and writes the loss to pinned host memory).  Also reported: gem.HostPipeline,
-    # which double-buffers the next step's copy behind the current step from Python.
+    # host->device on libgem's copy stream into double-buffered staging -- so call k + 1's copy
+    # runs behind call k's kernels -- and writes the loss to pinned host memory).  Also
+    # reported: gem.HostPipeline, which double-buffers the next step's copy from Python, and the
+    # PCIe bound: the same bytes through one pinned host->device copy, measured here.
     e2e = None
     if not args.no_e2e:
         hsrc = [a.cpu().pin_memory() for a in (rot, shift, ctf, obs)]
@@ -394,6 +395,14 @@ def main():
                 t = float(tt.item())
             return t
 
+        # the PCIe roofline of the e2e path: one step's input bytes as one pinned H2D copy
+        hb = torch.empty(B * (9 + 2 + 8 + w.D * w.D), dtype=torch.float32, pin_memory=True)
+        db = torch.empty_like(hb, device=dev)
+        for _ in range(3):
+            db.copy_(hb, non_blocking=True)
+        h2d_ms = timed(lambda: [db.copy_(hb, non_blocking=True) for _ in range(10)]) / 10
+        h2d_gbs = hb.numel() * 4 / (h2d_ms * 1e-3) / 1e9
+        del hb, db
         for k in range(2):
             step(k, host=True, src=hsrc)
 
@@ -411,8 +420,14 @@ def main():
         e2e = {"value": world * B * args.steps / (ems / 1e3), "unit": "particles/s",
                "h2d_bytes_per_step": B * (9 + 2 + 8 + w.D * w.D) * 4, "d2h_bytes_per_step": (B + 1) * 8,
                "path": "C ABI gem_forward with gem_batch.memory = GEM_MEM_HOST (pinned host poses, CTFs, "
-                       "images copied inside every call; images on libgem's side stream) + gem_backward + "
-                       "all-reduce + gem_step",
+                       "images copied inside every call on libgem's copy stream, double-buffered across calls) "
+                       "+ gem_backward + all-reduce + gem_step",
+               "pcie": {"bound": "h2d", "h2d_gbs_measured": h2d_gbs,
+                        "achieved_gbs": B * (9 + 2 + 8 + w.D * w.D) * 4 * args.steps / (ems * 1e-3) / 1e9,
+                        "frac": (B * (9 + 2 + 8 + w.D * w.D) * 4 * args.steps / (ems * 1e-3) / 1e9) / h2d_gbs,
+                        "ceiling_particles_per_s": world * h2d_gbs * 1e9 / (4 * (9 + 2 + 8 + w.D * w.D)),
+                        "note": "one step's input bytes as a single pinned host->device copy, timed here; the "
+                                "e2e value cannot exceed ceiling_particles_per_s with fp32 images"},
                "host_pipeline": {"value": world * B * args.steps / (pms / 1e3), "unit": "particles/s",
                                  "path": "gem.HostPipeline: the next step's inputs copied on a Python side "
                                          "stream, double-buffered behind the current step"}}

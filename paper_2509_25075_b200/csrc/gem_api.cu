@@ -122,10 +122,10 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.ctf_par = take(ctf_par_bytes() * Bm);
   L.stats = take(sizeof(DevStats));
   L.ticket = take(64);   // persistent-kernel work tickets (self-resetting; zeroed at init)
-  L.stage_rot = take(sizeof(float) * 9 * Bm);
-  L.stage_shift = take(sizeof(float) * 2 * Bm);
-  L.stage_ctf = take(sizeof(float) * 8 * Bm);
-  L.stage_obs = take(sizeof(float) * Bm * D * D);
+  L.stage_rot = take(sizeof(float) * 2 * 9 * Bm);   // the staging is double-buffered across calls
+  L.stage_shift = take(sizeof(float) * 2 * 2 * Bm);
+  L.stage_ctf = take(sizeof(float) * 2 * 8 * Bm);
+  L.stage_obs = take(sizeof(float) * 2 * Bm * D * D);
   L.stage_loss = take(sizeof(double) * (Bm + 1));
   L.cufft_work = take(cufft_bytes);
   L.cufft_work2 = take(cufft_bytes);
@@ -309,7 +309,13 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_ctf, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->ev_loss, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&ctx->ev_loss, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_small, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_obs_free[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_obs_free[1], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_sfree[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_sfree[1], cudaEventDisableTiming) != cudaSuccess) {
     delete ctx;
     return GEM_E_CUDA;
   }
@@ -349,6 +355,17 @@ gem_status gem_destroy(gem_ctx *ctx) {
     cudaEventDestroy(ctx->ev_ctf);
     cudaEventDestroy(ctx->ev_loss);
   }
+  if (ctx->copy) {
+    cudaStreamSynchronize(ctx->copy);
+    cudaStreamDestroy(ctx->copy);
+  }
+  for (int k = 0; k < ctx->n_ev_obs; ++k) cudaEventDestroy(ctx->ev_obs[k]);
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->ev_obs_free[k]) cudaEventDestroy(ctx->ev_obs_free[k]);
+    if (ctx->ev_sfree[k]) cudaEventDestroy(ctx->ev_sfree[k]);
+  }
+  if (ctx->ev_small) cudaEventDestroy(ctx->ev_small);
+  free(ctx->ev_obs);
   for (int k = 0; k < 2 * ctx->prof_cap; ++k) cudaEventDestroy(ctx->prof_ev[k]);
   free(ctx->prof_ev);
   free(ctx->prof_kind);
@@ -406,24 +423,55 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
   const CfgDev &c = ctx->dc;
   const Layout &L = ctx->L;
   const size_t D = (size_t)c.D;
-  float *rot = at<float>(ctx, L.stage_rot);
   const float *shift = batch->shift, *ctf = batch->ctf, *obs = batch->observed;
   const bool host = batch->memory == GEM_MEM_HOST;
-  // the rotation is kept in the workspace for gem_backward
-  CK(cudaMemcpyAsync(rot, batch->rot, sizeof(float) * 9 * B, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
-  if (host) {
-    // poses on the compute stream (the splat needs them first); the CTF parameters and the
-    // observed images (4 D^2 bytes per particle, the bulk of the input) on the internal side
-    // stream, where their only consumers (CTF constants, the observations' R2C) run: that copy
-    // overlaps the splat, binning and render of the compute stream
-    CK(cudaMemcpyAsync(at<float>(ctx, L.stage_shift), shift, sizeof(float) * 2 * B, cudaMemcpyHostToDevice, s));
-    CK(cudaEventRecord(ctx->ev_fork, s));
-    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-    CK(cudaMemcpyAsync(at<float>(ctx, L.stage_ctf), ctf, sizeof(float) * 8 * B, cudaMemcpyHostToDevice, ctx->side));
-    CK(cudaMemcpyAsync(at<float>(ctx, L.stage_obs), obs, sizeof(float) * B * D * D, cudaMemcpyHostToDevice, ctx->side));
-    shift = at<float>(ctx, L.stage_shift);
-    ctf = at<float>(ctx, L.stage_ctf);
-    obs = at<float>(ctx, L.stage_obs);
+  // The staging (rotations, kept for gem_backward; in host mode also the shifts, CTFs and
+  // images) is double-buffered across calls: this call uses half h.  Half 1 - h was the
+  // previous call's: the compute stream reaching this point means its backward has run.
+  const int h = ctx->obs_half;
+  ctx->obs_half ^= 1;
+  const size_t Bm = (size_t)ctx->cfg.max_batch;
+  float *rot = at<float>(ctx, L.stage_rot) + (size_t)h * 9 * Bm;
+  ctx->rot_cur = rot;
+  CK(cudaEventRecord(ctx->ev_sfree[1 - h], s));
+  if (!host) {
+    CK(cudaMemcpyAsync(rot, batch->rot, sizeof(float) * 9 * B, cudaMemcpyDeviceToDevice, s));
+  } else {
+    // Every host->device copy runs on the internal copy stream (none on the compute stream,
+    // where a small copy could queue behind the images of the next call), after the last
+    // readers of half h: the compute stream two calls back (ev_sfree) and that call's image
+    // R2Cs on the side stream (ev_obs_free).  Poses and CTFs first (the compute stream waits
+    // for them), then the images wave by wave (4 D^2 bytes per particle, the bulk of the
+    // input), one event per wave: their R2C on the side stream waits for its wave only.  A
+    // caller that enqueues its steps back to back gets call k + 1's inputs copied while call k
+    // computes.
+    const int nw = (B + ctx->W - 1) / ctx->W;
+    if (ctx->n_ev_obs < nw) {
+      cudaEvent_t *ne = (cudaEvent_t *)realloc(ctx->ev_obs, sizeof(cudaEvent_t) * nw);
+      if (!ne) return GEM_E_CUDA;
+      ctx->ev_obs = ne;
+      for (; ctx->n_ev_obs < nw; ++ctx->n_ev_obs)
+        CK(cudaEventCreateWithFlags(&ctx->ev_obs[ctx->n_ev_obs], cudaEventDisableTiming));
+    }
+    float *sshift = at<float>(ctx, L.stage_shift) + (size_t)h * 2 * Bm;
+    float *sctf = at<float>(ctx, L.stage_ctf) + (size_t)h * 8 * Bm;
+    float *sobs = at<float>(ctx, L.stage_obs) + (size_t)h * Bm * D * D;
+    CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_sfree[h], 0));
+    CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_obs_free[h], 0));
+    CK(cudaMemcpyAsync(rot, batch->rot, sizeof(float) * 9 * B, cudaMemcpyHostToDevice, ctx->copy));
+    CK(cudaMemcpyAsync(sshift, shift, sizeof(float) * 2 * B, cudaMemcpyHostToDevice, ctx->copy));
+    CK(cudaMemcpyAsync(sctf, ctf, sizeof(float) * 8 * B, cudaMemcpyHostToDevice, ctx->copy));
+    CK(cudaEventRecord(ctx->ev_small, ctx->copy));
+    for (int w = 0; w < nw; ++w) {
+      const int q0 = w * ctx->W, qn = B - q0 < ctx->W ? B - q0 : ctx->W;
+      CK(cudaMemcpyAsync(sobs + q0 * D * D, obs + q0 * D * D, sizeof(float) * qn * D * D, cudaMemcpyHostToDevice,
+                         ctx->copy));
+      CK(cudaEventRecord(ctx->ev_obs[w], ctx->copy));
+    }
+    CK(cudaStreamWaitEvent(s, ctx->ev_small, 0));
+    shift = sshift;
+    ctf = sctf;
+    obs = sobs;
   }
   DevStats *st = at<DevStats>(ctx, L.stats);
   CK(cudaMemsetAsync(st, 0, sizeof(DevStats), s));
@@ -450,6 +498,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     CK(cudaEventRecord(ctx->ev_fork, s));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     CKF(cufftSetStream(r2c_obs, ctx->side));
+    if (host) CK(cudaStreamWaitEvent(ctx->side, ctx->ev_obs[p0 / ctx->W], 0));
     {
       Prof p(ctx, ctx->side, P_FFT_OBS);
       CKF(cufftExecR2C(r2c_obs, (cufftReal *)(obs + p0 * DD), (cufftComplex *)so));
@@ -520,6 +569,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
       CK(cudaGetLastError());
     }
   }
+  if (host) CK(cudaEventRecord(ctx->ev_obs_free[h], ctx->side));   // its images' R2Cs are enqueued above
   ctx->last_p0 = p0 - ctx->W;
   ctx->last_nb = nb;
   // the per-particle loss reduction (and the host copy of the loss) runs on the side stream,
@@ -549,7 +599,7 @@ gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_
   if (!ctx->fused) {   // one batch: backward, then chunk sums reduced and finalized in one kernel
     {
       Prof p(ctx, s, P_RENDER_BWD);
-      launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<float>(ctx, L.dldi), at<float>(ctx, L.stage_rot),
+      launch_render_bwd(c, ctx->last_B, at<SplatRec>(ctx, L.rec), at<float>(ctx, L.dldi), ctx->rot_cur,
                         at<float>(ctx, L.slots), s, ctx->launches);
       CK(cudaGetLastError());
     }

@@ -94,6 +94,14 @@ struct gem_ctx {
   cufftHandle plan_il[8];   // C2C of the packed dL/dI row pairs (row path only, else 0)
   cudaStream_t side;   // internal stream: observed-image R2C overlapped with splat/bin/render
   cudaEvent_t ev_fork, ev_join, ev_ctf, ev_loss;   // side-stream fork / join points
+  cudaStream_t copy = nullptr;   // host mode: the observed images' H2D, wave by wave
+  cudaEvent_t *ev_obs = nullptr;   // one per wave: its images are on the device
+  int n_ev_obs = 0;
+  int obs_half = 0;   // the half of the double-buffered staging the next gem_forward uses
+  cudaEvent_t ev_obs_free[2] = {nullptr, nullptr};   // the side stream's last reads of each half are done
+  cudaEvent_t ev_sfree[2] = {nullptr, nullptr};      // the compute stream's last reads of each half are done
+  cudaEvent_t ev_small = nullptr;                    // host mode: poses and CTFs are on the device
+  float *rot_cur = nullptr;                          // the last forward's staged rotations (gem_backward)
   int n_plans;
   int fwd_live;        // a forward's lists/records/dL/dI are valid
   int last_B;
