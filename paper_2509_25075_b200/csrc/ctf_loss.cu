@@ -226,6 +226,42 @@ __device__ __forceinline__ void fft_col(float2 (&v)[R1], int t, float2 *sb, cons
   __syncwarp();
 }
 
+// inverse (unnormalised) DFT of one column held in fft_col's output order, v[s R2 + k2] =
+// Y[(t S + s) + R1 k2]; on return v[n1] = y[R2 n1 + t] = sum_k Y[k] W_D^(-(R2 n1 + t) k) (natural
+// order: no reordering pass).  With n = R2 n1 + n2 and k = k1 + R1 k2, W_D^(nk) = W_R1^(n1 k1)
+// W_D^(n2 k1) W_R2^(n2 k2): R2-point DFTs over k2 in registers, twiddles, one transpose through
+// shared memory, R1-point DFTs over k1 in registers -- the forward DFT of conj(Y), conjugated.
+template <int R1, int R2>
+__device__ __forceinline__ void fft_col_inv(float2 (&v)[R1], int t, float2 *sb, const float2 *__restrict__ tw) {
+  constexpr int S = R1 / R2, P = R2 + 1;
+  constexpr int D = R1 * R2;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    float2 u[R2];
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) u[k2] = make_float2(v[s * R2 + k2].x, -v[s * R2 + k2].y);
+    dft_reg<R2>(u);   // u[n2] = sum_k2 conj(Y)[k1 + R1 k2] W_R2^(n2 k2), k1 = t S + s
+    const int k1 = t * S + s;
+    const float2 w1 = tw[k1 & (D - 1)];   // W_D^(k1), then W_D^(n2 k1) by recurrence
+    float2 w = w1;
+#pragma unroll
+    for (int n2 = 1; n2 < R2; ++n2) {
+      const float2 x = u[n2];
+      u[n2] = make_float2(x.x * w.x - x.y * w.y, x.x * w.y + x.y * w.x);
+      w = make_float2(w.x * w1.x - w.y * w1.y, w.x * w1.y + w.y * w1.x);
+    }
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) sb[k1 * P + n2] = u[n2];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) v[k1] = sb[k1 * P + t];
+  __syncwarp();
+  dft_reg<R1>(v);
+#pragma unroll
+  for (int n1 = 0; n1 < R1; ++n1) v[n1].y = -v[n1].y;
+}
+
 constexpr int kColThreads = 128;
 
 template <int R1, int R2>
@@ -286,68 +322,39 @@ __global__ void __launch_bounds__(kColThreads) k_ctf_colspec(CfgDev c, const Ctf
     f[q] = make_float2(gsc * C * Rr, gsc * C * Ri);
     so[q][threadIdx.x] = make_float2(C * F.x * ps, C * F.y * ps);
   }
-  // inverse column DFT (unnormalised) = conj(DFT(conj(.))), back into row-spectrum order
-  auto inverse_store = [&](float2 (&v)[R1], float2 *dst) {
-#pragma unroll
-    for (int q = 0; q < R1; ++q) {
-      const int ky = (t * S + q / R2) + R1 * (q % R2);
-      sb[g][ky] = make_float2(v[q].x, -v[q].y);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int n1 = 0; n1 < R1; ++n1) v[n1] = sb[g][R2 * n1 + t];
-    __syncwarp();
-    fft_col<R1, R2>(v, t, sb[g], tw);
-    if (act) {
-#pragma unroll
-      for (int q = 0; q < R1; ++q) {
-        const int row = (t * S + q / R2) + R1 * (q % R2);
-        dst[col + (size_t)row * Hx] = make_float2(v[q].x, -v[q].y);
-      }
-    }
-  };
+  // inverse column DFTs in fft_col's output order (fft_col_inv): thread t ends with the rows
+  // R2 n1 + t, n1 = 0 .. R1 - 1, of column kx
   // gradient: rows (2m, 2m + 1) of the row spectrum, A and B, packed as one complex row
   // Z_m = A + i B over all D columns (A[D - kx] = conj A[kx]); the inverse C2C of Z_m is then
   // (g[2m][u], g[2m + 1][u]) interleaved: the layout k_render_bwd reads.  The imaginary parts
-  // at kx = 0 and D/2 are dropped (what a C2R of the Hermitian half spectrum computes).
+  // at kx = 0 and D/2 are dropped (what a C2R of the Hermitian half spectrum computes).  Row
+  // R2 n1 + t pairs with row R2 n1 + (t ^ 1), held by lane t ^ 1 of the group.
   {
-#pragma unroll
-    for (int q = 0; q < R1; ++q) {
-      const int ky = (t * S + q / R2) + R1 * (q % R2);
-      sb[g][ky] = make_float2(f[q].x, -f[q].y);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int n1 = 0; n1 < R1; ++n1) f[n1] = sb[g][R2 * n1 + t];
-    __syncwarp();
-    fft_col<R1, R2>(f, t, sb[g], tw);   // conj(f[q]) = row-spectrum value of row(q), column kx
+    fft_col_inv<R1, R2>(f, t, sb[g], tw);
     float2 *zi = zout + (size_t)i * (D / 2) * D;
-    auto put = [&](int m, float2 A, float2 B) {   // A = row 2m, B = row 2m + 1 (column kx)
-      if (kx == 0 || nx) {
-        zi[(size_t)m * D + kx] = make_float2(A.x, B.x);
-      } else {
-        zi[(size_t)m * D + kx] = make_float2(A.x - B.y, A.y + B.x);
-        zi[(size_t)m * D + (D - kx)] = make_float2(A.x + B.y, B.x - A.y);
-      }
-    };
-    if constexpr (S == 2) {   // row(q) = 2t + R1 q for q < R2, its partner row(q + R2) = row(q) + 1
 #pragma unroll
-      for (int q = 0; q < R2; ++q)
-        if (act)
-          put(t + (R1 / 2) * q, make_float2(f[q].x, -f[q].y), make_float2(f[q + R2].x, -f[q + R2].y));
-    } else {   // S == 1: row(q) = t + R1 q, the partner row is in lane t ^ 1 of the group
-#pragma unroll
-      for (int q = 0; q < R1; ++q) {
-        const float2 mine = make_float2(f[q].x, -f[q].y);
-        const float2 other = make_float2(__shfl_xor_sync(0xffffffffu, mine.x, 1), __shfl_xor_sync(0xffffffffu, mine.y, 1));
-        if (act && !(t & 1)) put((t >> 1) + (R1 / 2) * q, mine, other);
+    for (int n1 = 0; n1 < R1; ++n1) {
+      const float2 mine = f[n1];
+      const float2 other = make_float2(__shfl_xor_sync(0xffffffffu, mine.x, 1), __shfl_xor_sync(0xffffffffu, mine.y, 1));
+      if (act && !(t & 1)) {
+        const int m = (R2 * n1 + t) >> 1;   // A = row 2m (mine), B = row 2m + 1 (other)
+        if (kx == 0 || nx) {
+          zi[(size_t)m * D + kx] = make_float2(mine.x, other.x);
+        } else {
+          zi[(size_t)m * D + kx] = make_float2(mine.x - other.y, mine.y + other.x);
+          zi[(size_t)m * D + (D - kx)] = make_float2(mine.x + other.y, other.x - mine.y);
+        }
       }
     }
   }
   if (spred) {
 #pragma unroll
     for (int q = 0; q < R1; ++q) f[q] = so[q][threadIdx.x];
-    inverse_store(f, spred);
+    fft_col_inv<R1, R2>(f, t, sb[g], tw);
+    if (act) {
+#pragma unroll
+      for (int n1 = 0; n1 < R1; ++n1) spred[col + (size_t)(R2 * n1 + t) * Hx] = f[n1];
+    }
   }
   double ls = act ? (double)lsum : 0.0;
 #pragma unroll
