@@ -42,7 +42,8 @@ def make_case(wname="T", B=4, seed=0, N=None, D=None, state="steady", morton=Tru
     return dict(w=w, params=(mr, ls, q), rot=rot, shift=shift, ctf=ctf, obs=obs, px=float(np.float32(w.px)))
 
 
-def run_gpu(gem, case, tile=8, want_lists=False, cap=0, host=False, fused=False, wave=0, zsort=False):
+def run_gpu(gem, case, tile=8, want_lists=False, cap=0, host=False, fused=False, wave=0, zsort=False,
+            want_pred=True):
     w = case["w"]
     B = case["rot"].shape[0]
     cfg = gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=B, tile=tile, list_capacity=cap,
@@ -56,12 +57,13 @@ def run_gpu(gem, case, tile=8, want_lists=False, cap=0, host=False, fused=False,
         mk = lambda a: torch.from_numpy(a).to(dev)
     rot, shift, ctf, obs = (mk(case[k]) for k in ("rot", "shift", "ctf", "obs"))
     proj = torch.empty(B, w.D, w.D, device=dev)
-    pred = torch.empty(B, w.D, w.D, device=dev)
+    pred = torch.empty(B, w.D, w.D, device=dev) if want_pred else None
     loss = st.forward(P, rot, shift, ctf, obs, proj=proj, pred=pred, host=host)
     grad = gem.SoA.zeros(w.N, dev)
     st.backward(P, grad)
     torch.cuda.synchronize()
-    out = dict(st=st, P=P, loss=loss.cpu().numpy().copy(), proj=proj.cpu().numpy(), pred=pred.cpu().numpy(),
+    out = dict(st=st, P=P, loss=loss.cpu().numpy().copy(), proj=proj.cpu().numpy(),
+               pred=pred.cpu().numpy() if want_pred else None,
                grad=grad.t.permute(1, 0, 2).reshape(w.N, 12).cpu().numpy(), grad_soa=grad)
     if want_lists:
         first = 0 if not fused else B - ((B - 1) % wave + 1)   # only the last wave is resident when fused
@@ -414,18 +416,21 @@ def test_forward_without_outputs(gem, orc, D):
         assert maxnorm_rel(ga[:, cols], o["grad"][:, cols]) < GRAD_TOL, name
 
 
-def test_R_config_full_size(gem, orc):
+@pytest.mark.parametrize("want_pred", [True, False])
+def test_R_config_full_size(gem, orc, want_pred):
     """BASELINE config R at full size (N = 50,000, D = 256, px = 1.31 A) in the bench's launch
     configuration (default 8x8 tiles, non-fused), one particle: bit-exact lists and the whole
     projection, prediction, loss and every gradient class against the un-culled fp64 oracle
-    (~3e9 Gaussian-pixel terms per pass on the host cores)."""
+    (~3e9 Gaussian-pixel terms per pass on the host cores); with and without predicted images
+    (the bench's call has none)."""
     case = make_case("R", B=1, seed=12)
-    g = run_gpu(gem, case, tile=8, want_lists=True)
+    g = run_gpu(gem, case, tile=8, want_lists=True, want_pred=want_pred)
     assert g["stats"]["status"] == 0, g["stats"]
     assert_lists_exact(orc, case, g["lists"], 8)
     o = oracle_out(orc, case)
     assert maxnorm_rel(g["proj"][0], o["proj"][0]) < IMG_TOL
-    assert maxnorm_rel(g["pred"][0], o["pred"][0]) < IMG_TOL
+    if want_pred:
+        assert maxnorm_rel(g["pred"][0], o["pred"][0]) < IMG_TOL
     assert abs(g["loss"][-1] - o["total"]) < LOSS_TOL * o["total"]
     for name, cols in CLASSES.items():
         assert maxnorm_rel(g["grad"][:, cols], o["grad"][:, cols]) < GRAD_TOL, name
@@ -438,7 +443,7 @@ def test_R_config_bench_batch_sampled(gem, orc):
     of the gradients of its four 64-particle quarters."""
     B = 256
     case = make_case("R", B=B, seed=13)
-    g = run_gpu(gem, case, tile=8)
+    g = run_gpu(gem, case, tile=8, want_pred=False)
     assert g["stats"]["status"] == 0, g["stats"]
     st = g["st"]
     for i in (0, 127, 255):
@@ -452,7 +457,7 @@ def test_R_config_bench_batch_sampled(gem, orc):
     for q in range(4):
         sl = slice(64 * q, 64 * q + 64)
         sub = dict(case, rot=case["rot"][sl], shift=case["shift"][sl], ctf=case["ctf"][sl], obs=case["obs"][sl])
-        parts.append(run_gpu(gem, sub, tile=8)["grad"].astype(np.float64))
+        parts.append(run_gpu(gem, sub, tile=8, want_pred=False)["grad"].astype(np.float64))
     tot = sum(parts)
     for name, cols in CLASSES.items():
         assert maxnorm_rel(g["grad"][:, cols], tot[:, cols]) < 1e-5, name
@@ -656,7 +661,7 @@ def test_X_config_sampled(gem, orc):
     for h in range(2):
         sl = slice(2 * h, 2 * h + 2)
         sub = dict(case, rot=case["rot"][sl], shift=case["shift"][sl], ctf=case["ctf"][sl], obs=case["obs"][sl])
-        parts.append(run_gpu(gem, sub, tile=8)["grad"].astype(np.float64))
+        parts.append(run_gpu(gem, sub, tile=8, want_pred=False)["grad"].astype(np.float64))
     tot = parts[0] + parts[1]
     for name, cols in CLASSES.items():
         assert maxnorm_rel(g["grad"][:, cols], tot[:, cols]) < 1e-5, name
