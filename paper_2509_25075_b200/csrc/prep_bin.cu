@@ -452,30 +452,27 @@ __global__ void __launch_bounds__(kPpThreads) k_scan_pp(const int *__restrict__ 
   block_excl_scan(pb, sw, pbase);
   const int *in = hist + (size_t)i * seg;
   int *out = base + (size_t)i * seg;
-  // scan order (t, chunk) over the [chunk][t] layout (the particle's 4 NT C bytes sit in L1):
-  // tiles of 4 kPpThreads items, 4 consecutive (t, chunk) items per thread, the running total
-  // carried between tiles
+  // scan order (t, chunk) over the [chunk][t] layout: thread tau owns tile t = t0 + tau of a
+  // block of kPpThreads tiles and its C chunk counts (coalesced across the threads for each
+  // chunk, all loads in flight); one block scan of the tiles' totals per block of tiles, the
+  // running total carried between blocks; the chunk starts re-read from L1
   int carry = pbase;
-  for (int f0 = 0; f0 < seg; f0 += 4 * kPpThreads) {
-    const int f = f0 + 4 * threadIdx.x;
-    int v[4], idx[4], tl[4];
-    int t = f / C, ch = f - t * C;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      idx[k] = ch * NT + t;
-      tl[k] = ch == 0 ? t : -1;   // the list's own start (chunk 0)
-      v[k] = f + k < seg ? __ldg(in + idx[k]) : 0;
-      if (++ch == C) { ch = 0; ++t; }
+  for (int t0 = 0; t0 < NT; t0 += kPpThreads) {
+    const int t = t0 + threadIdx.x;
+    int sum = 0;
+    if (t < NT) {
+#pragma unroll 8
+      for (int ch = 0; ch < C; ++ch) sum += __ldg(in + (size_t)ch * NT + t);
     }
     int total;
-    int run = block_excl_scan((v[0] + v[1]) + (v[2] + v[3]), sw, total);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (f + k < seg) {
-        out[idx[k]] = carry + run;
-        if (tl[k] >= 0) lst[(size_t)i * NT + tl[k]] = carry + run;
+    int run = carry + block_excl_scan(sum, sw, total);
+    if (t < NT) {
+      lst[(size_t)i * NT + t] = run;   // the list's own start (chunk 0)
+#pragma unroll 8
+      for (int ch = 0; ch < C; ++ch) {
+        out[(size_t)ch * NT + t] = run;
+        run += __ldg(in + (size_t)ch * NT + t);
       }
-      run += v[k];
     }
     carry += total;
   }
