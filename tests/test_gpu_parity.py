@@ -202,6 +202,38 @@ def test_host_memory_batch_matches_device(gem):
     assert np.array_equal(a["grad"], h["grad"])
 
 
+def test_host_memory_back_to_back_steps(gem):
+    """GEM_MEM_HOST steps enqueued back to back with no host synchronisation: call k + 1's inputs
+    are copied into the other half of the double-buffered staging while call k runs.  Each
+    step's loss and gradient (into its own gradient buffer) are bitwise those of the same batch
+    run alone from device memory, so no copy overwrote staging still in use (the rotations the
+    backward reads, the images the side stream transforms)."""
+    case = make_case("T", B=4, seed=6)
+    w = case["w"]
+    dev = torch.device("cuda", 0)
+    st = gem.GemStep(gem.GemConfig(D=w.D, pixel_size=case["px"], n_gauss=w.N, max_batch=4))
+    P = gem.SoA.from_arrays(*case["params"], device=dev)
+    rng = np.random.default_rng(3)
+    batches = []
+    for k in range(5):
+        perm = rng.permutation(4)
+        batches.append([np.ascontiguousarray(case[n][perm]) for n in ("rot", "shift", "ctf", "obs")])
+    hosts = [[torch.from_numpy(a).pin_memory() for a in bt] for bt in batches]
+    losses = [torch.empty(5, dtype=torch.float64, pin_memory=True) for _ in batches]
+    grads = [gem.SoA.zeros(w.N, dev) for _ in batches]
+    for k, bt in enumerate(hosts):
+        st.forward(P, *bt, loss=losses[k], host=True)
+        st.backward(P, grads[k])
+    torch.cuda.synchronize()
+    for k, bt in enumerate(batches):
+        ref_loss = st.forward(P, *(torch.from_numpy(a).to(dev) for a in bt))
+        ref = gem.SoA.zeros(w.N, dev)
+        st.backward(P, ref)
+        torch.cuda.synchronize()
+        assert np.array_equal(losses[k].numpy(), ref_loss.cpu().numpy()), k
+        assert torch.equal(grads[k].t, ref.t), k
+
+
 def test_adam_step_identical_gradient_input(gem, orc):
     case = make_case("T", B=2, seed=7)
     g = run_gpu(gem, case)
