@@ -3,7 +3,7 @@
 # ncu launch list of the bench command, --set full captures of the step's main kernels and of the
 # measured TMA variants.  Everything under gpurun_out/round2/ (summaries copied to profiles/r2/).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-TAG=${TAG:-r2b}
+TAG=${TAG:-r2c}
 O=gpurun_out/round2
 mkdir -p $O
 nvidia-smi > $O/nvidia-smi.txt 2>&1
@@ -37,4 +37,12 @@ python -c "from paper_2509_25075_b200 import build as b; b.build(force=True)" > 
 for a in "--config S" "--config P" "--batch 128" "--batch 512" "--state init"; do
   timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-volume $a > "$O/bench_$(echo $a | tr -d ' -')_$TAG.json" 2>/dev/null
 done
+# the volume query's launch list and one --set full capture of its render kernel
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/vol_launches_$TAG.csv python tools/vol_probe.py > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_vol_render|k_vol_stage" -s 6 -c 2 -o $O/full_vol_$TAG python tools/vol_probe.py > $O/ncu_vol.log 2>&1
+python tools/ncu_summary.py $O/full_vol_$TAG.ncu-rep 30 > $O/ncu_full_summary_vol_$TAG.txt 2>&1
+python tools/ncu_stalls.py $O/full_vol_$TAG.ncu-rep >> $O/ncu_full_summary_vol_$TAG.txt 2>&1
+# the e2e path: PCIe bandwidth and copy/compute interference
+python tools/h2d_bw.py > $O/h2d_bw_$TAG.txt 2>&1
+python tools/copy_interference.py > $O/copy_interference_$TAG.txt 2>&1
 tail -2 $O/pytest_gpu.log; tail -2 $O/smoke.log; tail -1 $O/bench_$TAG.err
