@@ -56,7 +56,7 @@ bool resolve(const gem_config *in, gem_config &c, CfgDev &d) {
   // the splat kernel keeps kFillWarps tile histograms plus a kChunk exact queue in shared memory
   // and the fill kFillWarps cursor arrays: the tile grid must fit (D <= 856 at 8x8 tiles,
   // D <= 1712 at 16x16)
-  if ((size_t)(4 * d.NT + kChunk) * sizeof(int) > 200 * 1024) return false;
+  if ((size_t)(kFillWarps * d.NT + kChunk) * sizeof(int) > 200 * 1024) return false;
   if (c.list_capacity <= 0)   // per wave (= per batch when not fused)
     c.list_capacity = (int64_t)c.wave * ((c.tile == 16 ? 6 : 12) * (int64_t)d.N + d.NT);
   if (c.list_capacity > 0x7fffffffll) c.list_capacity = 0x7fffffffll;
@@ -106,7 +106,7 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.rec = take(sizeof(SplatRec) * W * N);
   L.box = take(sizeof(uint2) * W * N);
   L.hist = take(sizeof(int) * ((size_t)L.n_hist + W));   // [i][t][chunk] counts, then per-particle totals
-  L.subcnt = take(sizeof(int) * (size_t)L.n_hist * 4);   // per fill-warp sub-chunk tile counts
+  L.subcnt = take(sizeof(int) * (size_t)L.n_hist * kFillWarps);   // per fill-warp sub-chunk tile counts
   L.base = take(sizeof(int) * (size_t)L.n_hist);                  // [i][chunk][t] (the fill's cursors)
   L.lst = take(sizeof(int) * ((size_t)W * d.NT + 1));              // list starts [i][t] + the total
   L.ids = take(sizeof(int) * (size_t)L.list_cap);

@@ -10,7 +10,14 @@
 
 namespace gem {
 
-constexpr int kChunk = 4096;          // Gaussians per binning chunk (a3)
+#ifndef GEM_KCHUNK
+#define GEM_KCHUNK 4096
+#endif
+constexpr int kChunk = GEM_KCHUNK;    // Gaussians per binning chunk (a3)
+#ifndef GEM_FILLW
+#define GEM_FILLW 4
+#endif
+constexpr int kFillWarps = GEM_FILLW; // k_fill warps per chunk (sub-chunks with their own tile counts)
 constexpr double kSqrt2Pi = 2.5066282746310002;
 constexpr float kLog2e = 1.4426950408889634f;
 

@@ -167,7 +167,7 @@ constexpr int kSplatThreads = 256;
 #ifndef GEM_SPLAT_PF
 #define GEM_SPLAT_PF 1
 #endif
-constexpr int kFillWarps = 4, kSub = kChunk / kFillWarps;   // k_fill warps per chunk, Gaussians per warp
+constexpr int kSub = kChunk / kFillWarps;   // Gaussians per k_fill warp
 
 template <bool PM>
 __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, const GaussPrep *__restrict__ prep,
