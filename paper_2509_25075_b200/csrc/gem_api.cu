@@ -106,7 +106,7 @@ Layout layout(const gem_config &c, const CfgDev &d, size_t cufft_bytes) {
   L.rec = take(sizeof(SplatRec) * W * N);
   L.box = take(sizeof(uint2) * W * N);
   L.hist = take(sizeof(int) * ((size_t)L.n_hist + W));   // [i][t][chunk] counts, then per-particle totals
-  L.subcnt = take(sizeof(int) * (size_t)L.n_hist * kFillWarps);   // per fill-warp sub-chunk tile counts
+  L.subcnt = take(sizeof(unsigned short) * (size_t)L.n_hist * kFillWarps);   // per fill-warp sub-chunk tile counts (16 bits)
   L.base = take(sizeof(int) * (size_t)L.n_hist);                  // [i][chunk][t] (the fill's cursors)
   L.lst = take(sizeof(int) * ((size_t)W * d.NT + 1));              // list starts [i][t] + the total
   L.ids = take(sizeof(int) * (size_t)L.list_cap);
@@ -508,16 +508,17 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     const float *rw = rot + 9 * (size_t)p0;
     const int64_t nh = (int64_t)nb * c.NT * c.C;
     int *ptot = hist + nh;   // per-particle entry totals (the splat adds, the scan reads)
+    unsigned short *hist16 = reinterpret_cast<unsigned short *>(hist);   // 16-bit counts (<= kChunk)
     CK(cudaMemsetAsync(ptot, 0, sizeof(int) * nb, s));
-    { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist, at<int>(ctx, L.subcnt), ptot, st, s,
+    { Prof p(ctx, s, P_SPLAT); launch_splat_count(c, nb, prep, (const float4 *)params->mean_rho, rw, shift + 2 * (size_t)p0, rec, box, hist16, at<unsigned short>(ctx, L.subcnt), ptot, st, s,
                          ctx->launches); CK(cudaGetLastError()); }
     {
       Prof p(ctx, s, P_SCAN);
-      launch_scan_pp(c, nb, hist, base, at<int>(ctx, L.lst), ptot, st, at<int>(ctx, L.ticket) + 8, s, ctx->launches);
+      launch_scan_pp(c, nb, hist16, base, at<int>(ctx, L.lst), ptot, st, at<int>(ctx, L.ticket) + 8, s, ctx->launches);
       CK(cudaGetLastError());
     }
     uint2 *zpair = (c.flags & GEM_FLAG_ZSORT) ? at<uint2>(ctx, L.zs_key) : nullptr;
-    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<int>(ctx, L.subcnt), ids, (const float4 *)params->mean_rho, rw, zpair, rec, s, ctx->launches); CK(cudaGetLastError()); }
+    { Prof p(ctx, s, P_FILL); launch_fill(c, nb, box, base, at<unsigned short>(ctx, L.subcnt), ids, (const float4 *)params->mean_rho, rw, zpair, rec, s, ctx->launches); CK(cudaGetLastError()); }
     if (zpair) {
       Prof p(ctx, s, P_ZSORT);
       launch_zsort(c, nb, at<int>(ctx, L.lst), (const float4 *)params->mean_rho, rw, ids, zpair, at<int>(ctx, L.zs_tmp),

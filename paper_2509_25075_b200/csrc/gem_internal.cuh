@@ -207,13 +207,13 @@ namespace gem {
 void launch_prep(const CfgDev &c, const float4 *mean_rho, const float4 *log_scale, const float4 *quat, GaussPrep *prep,
                  DevStats *st, cudaStream_t s, int &launches);
 void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
-                        const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, int *ptot, DevStats *st,
-                        cudaStream_t s, int &launches);
-void launch_scan_pp(const CfgDev &c, int B, const int *hist, int *base, int *lst, const int *ptot, DevStats *st,
+                        const float *shift, SplatRec *rec, uint2 *box, unsigned short *hist, unsigned short *subcnt,
+                        int *ptot, DevStats *st, cudaStream_t s, int &launches);
+void launch_scan_pp(const CfgDev &c, int B, const unsigned short *hist, int *base, int *lst, const int *ptot, DevStats *st,
                     int *tk, cudaStream_t s, int &launches);
 void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, DevStats *st, int64_t cap, cudaStream_t s,
                  int &launches);
-void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,
+void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const unsigned short *subcnt, int *ids,
                  const float4 *mean_rho, const float *rot, uint2 *zpair, const SplatRec *rec, cudaStream_t s,
                  int &launches);
 void launch_zsort(const CfgDev &c, int B, const int *base, const float4 *mean_rho, const float *rot, int *ids,

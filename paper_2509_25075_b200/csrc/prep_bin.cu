@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
                                                                const float *__restrict__ rot,
                                                                const float *__restrict__ shift,
                                                                SplatRec *__restrict__ rec, uint2 *__restrict__ box,
-                                                               int *__restrict__ hist, int *__restrict__ subcnt,
+                                                               unsigned short *__restrict__ hist,
+                                                               unsigned short *__restrict__ subcnt,
                                                                int *__restrict__ ptot, DevStats *__restrict__ st) {
   // [kFillWarps][NT] tile histograms of the chunk's kFillWarps sub-chunks (one per k_fill warp),
   // then the exact-path queue [kChunk]
@@ -332,17 +333,17 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
   for (int d = 16; d >= 1; d >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, d);
   if ((tid & 31) == 0 && pairs) atomicAdd(&st->pairs, (unsigned long long)pairs);
   __syncthreads();
-  int *sc = subcnt + ((size_t)i * c.C + ch) * kFillWarps * c.NT;
+  unsigned short *sc = subcnt + ((size_t)i * c.C + ch) * kFillWarps * c.NT;   // (counts <= kChunk: 16 bits)
   int ctot = 0;   // the chunk's entries, added to the particle's total (k_scan_pp's starts)
   for (int t = tid; t < c.NT; t += blockDim.x) {
     int tot = 0;
 #pragma unroll
     for (int w = 0; w < kFillWarps; ++w) {
       const int v = shist[w * c.NT + t];
-      sc[w * c.NT + t] = v;
+      sc[w * c.NT + t] = (unsigned short)v;
       tot += v;
     }
-    hist[((size_t)i * c.C + ch) * c.NT + t] = tot;   // [i][chunk][t]: coalesced
+    hist[((size_t)i * c.C + ch) * c.NT + t] = (unsigned short)tot;   // [i][chunk][t]: coalesced
     ctot += tot;
   }
 #pragma unroll
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int *__restrict__ out
 // flags (the fill never writes past the buffer; the step's outputs are then invalid, include/gem.h).
 constexpr int kPpThreads = 1024;
 
-__global__ void __launch_bounds__(kPpThreads) k_scan_pp(const int *__restrict__ hist, int *__restrict__ base,
+__global__ void __launch_bounds__(kPpThreads) k_scan_pp(const unsigned short *__restrict__ hist, int *__restrict__ base,
                                                         int *__restrict__ lst, int NT, int C, int B,
                                                         const int *__restrict__ ptot, int64_t cap, DevStats *st,
                                                         int *tk) {
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(kPpThreads) k_scan_pp(const int *__restrict__ 
   for (int b = threadIdx.x; b < i; b += kPpThreads) pb += __ldg(ptot + b);
   int pbase;
   block_excl_scan(pb, sw, pbase);
-  const int *in = hist + (size_t)i * seg;
+  const unsigned short *in = hist + (size_t)i * seg;
   int *out = base + (size_t)i * seg;
   // scan order (t, chunk) over the [chunk][t] layout: thread tau owns tile t = t0 + tau of a
   // block of kPpThreads tiles and its C chunk counts (coalesced across the threads for each
@@ -499,7 +500,7 @@ __global__ void __launch_bounds__(kPpThreads) k_scan_pp(const int *__restrict__ 
 template <bool ZK, bool PM>
 __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 *__restrict__ box,
                                                           const int *__restrict__ base,
-                                                          const int *__restrict__ subcnt, int *__restrict__ ids,
+                                                          const unsigned short *__restrict__ subcnt, int *__restrict__ ids,
                                                           const float4 *__restrict__ mean_rho,
                                                           const float *__restrict__ rot, uint2 *__restrict__ zpair,
                                                           const SplatRec *__restrict__ rec) {
@@ -512,7 +513,7 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(CfgDev c, const uint2 
   const uint2 *boxi = box + (size_t)i * c.N;
   // cursors: the chunk's offset of each tile plus the counts of the preceding sub-chunks (the
   // splat kernel counted each sub-chunk's entries per tile)
-  const int *sc = subcnt + ((size_t)i * c.C + ch) * kFillWarps * c.NT;
+  const unsigned short *sc = subcnt + ((size_t)i * c.C + ch) * kFillWarps * c.NT;
   for (int t = threadIdx.x; t < c.NT; t += blockDim.x) {
     int run = base[((size_t)i * c.C + ch) * c.NT + t];
 #pragma unroll
@@ -711,7 +712,8 @@ void launch_prep(const CfgDev &c, const float4 *mean_rho, const float4 *log_scal
 }
 
 void launch_splat_count(const CfgDev &c, int B, const GaussPrep *prep, const float4 *mean_rho, const float *rot,
-                        const float *shift, SplatRec *rec, uint2 *box, int *hist, int *subcnt, int *ptot, DevStats *st,
+                        const float *shift, SplatRec *rec, uint2 *box, unsigned short *hist, unsigned short *subcnt,
+                        int *ptot, DevStats *st,
                         cudaStream_t s, int &launches) {
   dim3 grid(c.C, B);
   const size_t smem = (kFillWarps * c.NT + kChunk) * sizeof(int);
@@ -737,14 +739,14 @@ void launch_scan(const int *in, int *out, int64_t n, int *blk, int64_t nblk, Dev
   launches += 3;
 }
 
-void launch_scan_pp(const CfgDev &c, int B, const int *hist, int *base, int *lst, const int *ptot, DevStats *st,
+void launch_scan_pp(const CfgDev &c, int B, const unsigned short *hist, int *base, int *lst, const int *ptot, DevStats *st,
                     int *tk, cudaStream_t s, int &launches) {
   k_scan_pp<<<B, kPpThreads, 0, s>>>(hist, base, lst, c.NT, c.C, B, ptot, c.cap, st, tk);
   ++launches;
 }
 
 
-void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const int *subcnt, int *ids,
+void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, const unsigned short *subcnt, int *ids,
                  const float4 *mean_rho, const float *rot, uint2 *zpair, const SplatRec *rec, cudaStream_t s,
                  int &launches) {
   dim3 grid(c.C, B);
