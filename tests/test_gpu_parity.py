@@ -200,6 +200,12 @@ def test_host_memory_batch_matches_device(gem):
     # the backward writes one slot per (particle, Gaussian) and reduces them in a fixed order:
     # no atomics, so the gradient is bitwise reproducible too
     assert np.array_equal(a["grad"], h["grad"])
+    # fused waves of 2 (and a ragged last wave of 1): each wave's images copied and awaited apart
+    case5 = make_case("T", B=5, seed=6)
+    af = run_gpu(gem, case5, fused=True, wave=2)
+    hf = run_gpu(gem, case5, fused=True, wave=2, host=True)
+    assert np.array_equal(af["proj"], hf["proj"]) and np.array_equal(af["loss"], hf["loss"])
+    assert np.array_equal(af["grad"], hf["grad"])
 
 
 def test_host_memory_back_to_back_steps(gem):
