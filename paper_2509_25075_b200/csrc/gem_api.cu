@@ -8,6 +8,8 @@
 
 #include "gem_internal.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 using namespace gem;
 
 namespace {
@@ -220,11 +222,14 @@ gem_status plan_for(gem_ctx *ctx, int B, cufftHandle *r2c, cufftHandle *c2r, cuf
 const char *kProfNames[P_COUNT] = {"prep", "splat_count", "scan", "fill", "render_fwd", "fft_r2c",
                                    "ctf_loss", "fft_c2r", "fft_r2c_obs", "render_bwd", "bwd_reduce", "finalize", "adam", "volume", "zsort"};
 
+// Every profiled region is also an NVTX range (host side, the enqueue of its kernels): an nsys
+// or ncu --nvtx run sees the step's phases by name; without a tool attached NVTX is a no-op.
 struct Prof {
   gem_ctx *ctx;
   cudaStream_t s;
   int rec;
   Prof(gem_ctx *c, cudaStream_t st, int kind) : ctx(c), s(st), rec(-1) {
+    nvtxRangePushA(kProfNames[kind]);
     if (!c->prof_on) return;
     if (c->prof_n >= c->prof_cap) {
       int ncap = c->prof_cap ? 2 * c->prof_cap : 256;
@@ -242,7 +247,14 @@ struct Prof {
   }
   ~Prof() {
     if (rec >= 0) cudaEventRecord(ctx->prof_ev[2 * rec + 1], s);
+    nvtxRangePop();
   }
+};
+
+// one NVTX range per C-ABI call
+struct NvtxCall {
+  explicit NvtxCall(const char *name) { nvtxRangePushA(name); }
+  ~NvtxCall() { nvtxRangePop(); }
 };
 
 #define CK(x)                                          \
@@ -410,6 +422,7 @@ int32_t gem_profile_read(gem_ctx *ctx, gem_kernel_time_t *out, int32_t cap) {
 
 gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *batch, double *loss, float *proj_out,
                        float *pred_out, gem_stream_t stream) {
+  NvtxCall nvtx_("gem_forward");
   if (!ctx || !soa_ok(params) || !batch || !loss) return GEM_E_INVALID;
   if (!batch->rot || !batch->shift || !batch->ctf || !batch->observed) return GEM_E_INVALID;
   const int B = batch->B;
@@ -588,6 +601,7 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
 }
 
 gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_stream_t stream) {
+  NvtxCall nvtx_("gem_backward");
   if (!ctx || !soa_ok(params) || !soa_ok(grad)) return GEM_E_INVALID;
   if (!soa_aligned(params) || !soa_aligned(grad)) return GEM_E_ALIGN;
   if (!ctx->fwd_live) return GEM_E_STATE;
@@ -623,6 +637,7 @@ gem_status gem_backward(gem_ctx *ctx, const gem_soa *params, gem_soa *grad, gem_
 
 gem_status gem_step(gem_ctx *ctx, gem_soa *params, const gem_soa *grad, gem_soa *m, gem_soa *v, int64_t t,
                     gem_stream_t stream) {
+  NvtxCall nvtx_("gem_step");
   if (!ctx || !soa_ok(params) || !soa_ok(grad) || !soa_ok(m) || !soa_ok(v) || t < 1) return GEM_E_INVALID;
   if (!soa_aligned(params) || !soa_aligned(grad) || !soa_aligned(m) || !soa_aligned(v)) return GEM_E_ALIGN;
   cudaStream_t s = (cudaStream_t)stream;
@@ -648,6 +663,7 @@ size_t gem_volume_scratch_bytes(const gem_ctx *ctx, int32_t Dv, float voxel_size
 
 gem_status gem_render_volume(gem_ctx *ctx, const gem_soa *params, int32_t Dv, float voxel_size, float *vol_out,
                              void *scratch, size_t scratch_bytes, gem_stream_t stream) {
+  NvtxCall nvtx_("gem_render_volume");
   if (!ctx || !soa_ok(params) || !vol_out || Dv < 2 || Dv > 4096 || !(voxel_size > 0.f)) return GEM_E_INVALID;
   if (!soa_aligned(params)) return GEM_E_ALIGN;
   const size_t need = volume_scratch_bytes(ctx->dc.N, Dv);
