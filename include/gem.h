@@ -134,8 +134,12 @@ enum { GEM_MEM_DEVICE = 0, GEM_MEM_HOST = 1 };
 typedef struct {
   int32_t B;              /* 1..max_batch                                                  */
   int32_t memory;         /* GEM_MEM_DEVICE, or GEM_MEM_HOST: the four arrays are pinned
-                             host memory, copied in-stream into the workspace, and the loss
-                             of gem_forward is written to a pinned host pointer             */
+                             host memory, copied asynchronously into the workspace (an
+                             internal copy stream; staging double-buffered across calls, so
+                             call k + 1's copy overlaps call k's kernels), and the loss of
+                             gem_forward is written to a pinned host pointer.  The host
+                             arrays must stay unchanged until `stream` has passed this call
+                             (e.g. an event recorded after it), as for any async copy     */
   const float *rot;       /* [B][9] row-major particle rotation P_i (world->camera = P_i^T) */
   const float *shift;     /* [B][2] in-plane translation t_i, Angstrom                      */
   const float *ctf;       /* [B][8] du, dv (A), astig angle (rad), kV, Cs (mm), amplitude
