@@ -506,18 +506,22 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
     gem_status ps = plan_for(ctx, nb, &r2c, &c2r, &r2c_obs, &c2r_il);
     if (ps != GEM_OK) return ps;
     // fork: the observed images' R2C and the per-particle CTF constants run on the internal side
-    // stream, overlapped with the splat / binning / render of this wave; joined before the
-    // CTF/loss kernel
-    CK(cudaEventRecord(ctx->ev_fork, s));
-    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-    CKF(cufftSetStream(r2c_obs, ctx->side));
-    if (host) CK(cudaStreamWaitEvent(ctx->side, ctx->ev_obs[p0 / ctx->W], 0));
-    {
-      Prof p(ctx, ctx->side, P_FFT_OBS);
-      CKF(cufftExecR2C(r2c_obs, (cufftReal *)(obs + p0 * DD), (cufftComplex *)so));
-    }
-    { Prof p(ctx, ctx->side, P_CTF_LOSS); launch_ctf_params(c, nb, ctf + 8 * (size_t)p0, ctx->ws + L.ctf_par, ctx->side, ctx->launches); CK(cudaGetLastError()); }
-    CK(cudaEventRecord(ctx->ev_join, ctx->side));
+    // stream, overlapped with the render of this wave; joined before the CTF/loss kernel.  (Forked
+    // at the wave's start instead, the R2C overlaps the splat, scan and fill and slows them: the
+    // same device-resident step, but 2.5 % less end to end with host inputs.)
+    auto fork_side = [&]() -> gem_status {
+      CK(cudaEventRecord(ctx->ev_fork, s));
+      CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      CKF(cufftSetStream(r2c_obs, ctx->side));
+      if (host) CK(cudaStreamWaitEvent(ctx->side, ctx->ev_obs[p0 / ctx->W], 0));
+      {
+        Prof p(ctx, ctx->side, P_FFT_OBS);
+        CKF(cufftExecR2C(r2c_obs, (cufftReal *)(obs + p0 * DD), (cufftComplex *)so));
+      }
+      { Prof p(ctx, ctx->side, P_CTF_LOSS); launch_ctf_params(c, nb, ctf + 8 * (size_t)p0, ctx->ws + L.ctf_par, ctx->side, ctx->launches); CK(cudaGetLastError()); }
+      CK(cudaEventRecord(ctx->ev_join, ctx->side));
+      return GEM_OK;
+    };
     const float *rw = rot + 9 * (size_t)p0;
     const int64_t nh = (int64_t)nb * c.NT * c.C;
     int *ptot = hist + nh;   // per-particle entry totals (the splat adds, the scan reads)
@@ -537,6 +541,10 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
       launch_zsort(c, nb, at<int>(ctx, L.lst), (const float4 *)params->mean_rho, rw, ids, zpair, at<int>(ctx, L.zs_tmp),
                    at<int>(ctx, L.zs_queue), s, ctx->launches);
       CK(cudaGetLastError());
+    }
+    {   // the side stream's work starts with the render (see fork_side)
+      const gem_status fs = fork_side();
+      if (fs != GEM_OK) return fs;
     }
     float *proj = proj_out ? proj_out + p0 * DD : at<float>(ctx, L.proj);
     { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, at<int>(ctx, L.lst), ids, proj, at<int>(ctx, L.ticket), s, ctx->launches); CK(cudaGetLastError()); }

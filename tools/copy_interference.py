@@ -74,3 +74,20 @@ for _ in range(20):
 t1 = time.perf_counter()
 torch.cuda.synchronize()
 print("device mode: %.3f ms per step to enqueue on the host" % ((t1 - t0) * 1e3 / 20))
+
+# per-phase device time (events on the launching streams) of device-mode vs host-mode steps
+g = tr.step_ctx
+def phases(host):
+    g.profile(True)
+    for _ in range(20):
+        if host:
+            tr.train_step(*hsrc, host=True, loss=hloss)
+        else:
+            tr.train_step(rot, sh, ctf, obs)
+    torch.cuda.synchronize()
+    g.profile(False)
+    return {k: v[1] / v[0] for k, v in g.profile_read().items()}
+dv, hv = phases(False), phases(True)
+print("phase            device-mode  host-mode  (ms per launch)")
+for k in dv:
+    print("%-16s %10.4f %10.4f" % (k, dv[k], hv.get(k, float("nan"))))
