@@ -117,6 +117,48 @@ __global__ void __launch_bounds__(10 * kRfG) k_reduce_finalize(int nchunk, int N
              make_float4(v[8], v[9], 0.f, 0.f), prep, mr, ls, q, g_mr, g_ls, g_q, st);
 }
 
+// The same with 128-bit loads (N % 4 == 0): one block per 128 Gaussians, warp k sums component k
+// of four Gaussians per lane (float4 rows), eight chunks in flight; then 128 threads finalize.
+constexpr int kRf4 = 128;
+__global__ void __launch_bounds__(320) k_reduce_finalize4(int nchunk, int N, int no_rot, const float *__restrict__ slots,
+                                                         const GaussPrep *__restrict__ prep,
+                                                         const float4 *__restrict__ mr, const float4 *__restrict__ ls,
+                                                         const float4 *__restrict__ q, float4 *__restrict__ g_mr,
+                                                         float4 *__restrict__ g_ls, float4 *__restrict__ g_q,
+                                                         DevStats *st) {
+  __shared__ float sv[10][kRf4];
+  const int lane = threadIdx.x & 31, k = threadIdx.x >> 5, j0 = blockIdx.x * kRf4 + 4 * lane;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j0 < N) {   // (N % 4 == 0: the four Gaussians are all in range)
+    const float4 *src = reinterpret_cast<const float4 *>(slots + (size_t)k * N + j0);
+    const size_t cs = (size_t)10 * N / 4;   // one chunk, in float4
+    int ch = 0;
+    for (; ch + 8 <= nchunk; ch += 8) {   // eight loads in flight, added in chunk order
+      float4 a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = __ldg(src + (size_t)(ch + u) * cs);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc.x += a[u].x; acc.y += a[u].y; acc.z += a[u].z; acc.w += a[u].w;
+      }
+    }
+    for (; ch < nchunk; ++ch) {
+      const float4 a = __ldg(src + (size_t)ch * cs);
+      acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+    }
+  }
+  *reinterpret_cast<float4 *>(&sv[k][4 * lane]) = acc;
+  __syncthreads();
+  const int jj = threadIdx.x, j = blockIdx.x * kRf4 + jj;
+  if (jj >= kRf4 || j >= N) return;
+  float v[10];
+#pragma unroll
+  for (int m = 0; m < 10; ++m) v[m] = sv[m][jj];
+  const float rho = mr[j].w;
+  finalize_j(j, no_rot, make_float4(rho != 0.f ? v[0] / rho : 0.f, v[1], v[2], v[3]), make_float4(v[4], v[5], v[6], v[7]),
+             make_float4(v[8], v[9], 0.f, 0.f), prep, mr, ls, q, g_mr, g_ls, g_q, st);
+}
+
 __device__ __forceinline__ float adam1(float p, float g, float &m, float &v, float lr, float b1, float b2, float eps,
                                        float bc1, float bc2) {
   m = b1 * m + (1.f - b1) * g;
@@ -172,9 +214,13 @@ __global__ void __launch_bounds__(256) k_adam(int N, AdamArgs A) {
 void launch_reduce_finalize(const CfgDev &c, int B, const float *slots, const GaussPrep *prep, const float4 *mean_rho,
                             const float4 *log_scale, const float4 *quat, float4 *g_mr, float4 *g_ls, float4 *g_q, DevStats *st, cudaStream_t s,
                             int &launches) {
-  k_reduce_finalize<<<(c.N + kRfG - 1) / kRfG, 10 * kRfG, 0, s>>>(bwd_chunks(B), c.N,
-                                                                  c.flags & GEM_FLAG_NO_ROTATION ? 1 : 0, slots, prep,
-                                                                  mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
+  const int no_rot = c.flags & GEM_FLAG_NO_ROTATION ? 1 : 0;
+  if (c.N % 4 == 0)
+    k_reduce_finalize4<<<(c.N + kRf4 - 1) / kRf4, 320, 0, s>>>(bwd_chunks(B), c.N, no_rot, slots, prep, mean_rho,
+                                                               log_scale, quat, g_mr, g_ls, g_q, st);
+  else
+    k_reduce_finalize<<<(c.N + kRfG - 1) / kRfG, 10 * kRfG, 0, s>>>(bwd_chunks(B), c.N, no_rot, slots, prep,
+                                                                    mean_rho, log_scale, quat, g_mr, g_ls, g_q, st);
   ++launches;
 }
 
