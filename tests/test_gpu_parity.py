@@ -312,6 +312,24 @@ def test_render_volume_full_grid(gem, orc):
     assert maxnorm_rel(vol, ref) < IMG_TOL
 
 
+def test_render_volume_wide_gaussians(gem, orc):
+    """Gaussians whose voxel boxes span up to 5^3 bricks: the count pass takes a slot for the
+    first 8 bricks of each, the rest go through the second counter and the fill's atomic cursor
+    (volume.cu k_vol_prep / k_vol_fill); against the oracle, and bitwise reproducible."""
+    case = make_case("T", B=1, seed=73, N=60, D=32)
+    mr, ls, q = case["params"]
+    ls = ls.copy()
+    ls[:, :3] = np.log(np.float32(6.0)) + 0.2 * np.random.default_rng(2).standard_normal((60, 3)).astype(np.float32)
+    vs = 2.0   # sigma ~ 3 voxels: boxes ~ 18 voxels, 3-4 bricks per axis
+    st = gem.GemStep(gem.GemConfig(D=32, pixel_size=vs, n_gauss=60, max_batch=1))
+    P = gem.SoA.from_arrays(mr, ls, q, device=st.device)
+    a = st.render_volume(P, 64, vs).cpu().numpy()
+    b = st.render_volume(P, 64, vs).cpu().numpy()
+    assert np.array_equal(a, b)
+    ref = orc.volume((mr, ls, q), 64, vs, masked=True)
+    assert maxnorm_rel(a, ref) < IMG_TOL
+
+
 def test_render_volume_large_grid(gem, orc):
     """Dv = 416 (> 2^17 bricks): the general multi-block scan, every brick's slot taken by the
     fill's atomic (no pre-taken slots), against the oracle."""
