@@ -19,6 +19,11 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float rcp_approx(float x) {   // 1 ulp: the amplitude and conic only
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // Rounding on the FMA/ALU pipes instead of the XU (FRND / F2I run at 16 lanes/clk/SM): for
 // |x| < 2^22, x + 1.5 * 2^23 rounds x to the nearest integer in the low mantissa bits.
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
     const float x01 = fmaf(p[0], q[1], -p[1] * q[0]), x02 = fmaf(p[0], q[2], -p[2] * q[0]),
                 x12 = fmaf(p[1], q[2], -p[2] * q[1]);
     const float d2f = fmaf(s3[0] * s3[1], x01 * x01, fmaf(s3[0] * s3[2], x02 * x02, s3[1] * s3[2] * x12 * x12));
-    const float ampf = m4.w * 2.5066282746310002f * rsqrt_approx(d2f * __frcp_rn(s3[0] * s3[1] * s3[2]));
+    const float ampf = m4.w * 2.5066282746310002f * rsqrt_approx(d2f * rcp_approx(s3[0] * s3[1] * s3[2]));
     const float cx = (float)mxd, cy = (float)myd;
     const float rxp = kf * (Af * rsqrt_approx(Af)) * ipxf, ryp = kf * (Cf * rsqrt_approx(Cf)) * ipxf;
     const float fu0 = cx - rxp, fu1 = cx + rxp, fv0 = cy - ryp, fv1 = cy + ryp;
@@ -301,7 +306,8 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
     const bool okf = s3[0] >= 0.f && d2f > 0.f && fabsf(ampf) < 3e38f && fabsf(fu0) < 2e6f && fabsf(fu1) < 2e6f &&
                      fabsf(fv0) < 2e6f && fabsf(fv1) < 2e6f;
     const float ru0 = rint_fma(fu0), ru1 = rint_fma(fu1), rv0 = rint_fma(fv0), rv1 = rint_fma(fv1);
-    const bool near = nearint(fu0, ru0) || nearint(fu1, ru1) || nearint(fv0, rv0) || nearint(fv1, rv1) ||
+    // (bitwise ORs: one predicate chain, no short-circuit branches)
+    const bool near = nearint(fu0, ru0) | nearint(fu1, ru1) | nearint(fv0, rv0) | nearint(fv1, rv1) |
                       (tau > 0.0 && fabsf(fabsf(ampf) - tauf) <= 1e-4f * tauf);
     if (s3[0] >= 0.f && (!okf || near)) {   // deferred to the exact pass (compact, no warp divergence)
       queue[atomicAdd(&qn, 1)] = j;
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(kSplatThreads, 4) k_splat_count(CfgDev c, cons
     const int vlo = iround_fma(fminf(fmaxf(cv0, 0.f), Df));
     const int vhi = iround_fma(fmaxf(fminf(fv1f, Df - 1.f), -1.f));
     const bool vis = okf && fabsf(ampf) > tauf && ulo <= uhi && vlo <= vhi;
-    const float id2 = px2f / d2f;
+    const float id2 = px2f * rcp_approx(d2f);   // (d2f > 0 and ampf finite on this path)
     emit(j, vis, ulo, uhi, vlo, vhi, (float)__dsub_rn(mxd, i2d_magic(ulo)), (float)__dsub_rn(myd, i2d_magic(vlo)),
          Cf * id2, -Bf * id2, Af * id2, ampf);
   }

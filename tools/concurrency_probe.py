@@ -78,3 +78,26 @@ def stag(split):
     s0.wait_event(ea); s0.wait_event(eb)
 print("2 x B=128 two streams, raw calls: %.3f ms per 256 particles" % timeit(lambda: stag(False)))
 print("2 x B=128 two streams, b's forward after a's: %.3f ms per 256 particles" % timeit(lambda: stag(True)))
+
+def lanes():
+    # the library-internal two-lane step this probe models: both halves' forward + backward on two
+    # streams, then one Adam (the gradient merge, ~3 us, is left out)
+    ev = torch.cuda.Event()
+    ev.record(s0)
+    sa.wait_event(ev); sb.wait_event(ev)
+    ga, gb = ta.step_ctx, tb.step_ctx
+    with torch.cuda.stream(sa):
+        ga.forward(ta.params, rot[:128], sh[:128], ctf[:128], obs[:128])
+        ga.backward(ta.params, ta.grad)
+    with torch.cuda.stream(sb):
+        gb.forward(tb.params, rot[128:], sh[128:], ctf[128:], obs[128:])
+        gb.backward(tb.params, tb.grad)
+    ea, eb = torch.cuda.Event(), torch.cuda.Event()
+    ea.record(sa); eb.record(sb)
+    s0.wait_event(ea); s0.wait_event(eb)
+    ta.t += 1
+    ga.stream = s0
+    ga.step(ta.params, ta.grad, ta.m, ta.v, ta.t)
+    ga.stream = sa
+print("two lanes + one Adam: %.3f ms per 256 particles" % timeit(lanes))
+print("B=256 one context (again): %.3f ms per 256 particles" % timeit(lambda: full.train_step(rot, sh, ctf, obs)))
