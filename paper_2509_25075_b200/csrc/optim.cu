@@ -159,19 +159,26 @@ __global__ void __launch_bounds__(320) k_reduce_finalize4(int nchunk, int N, int
              make_float4(v[8], v[9], 0.f, 0.f), prep, mr, ls, q, g_mr, g_ls, g_q, st);
 }
 
+// MUFU square root and reciprocal (a few ulp in the step lr m^ / (sqrt(v^) + eps): far below the
+// 1e-6 parity with the fp64 optimizer, and no IEEE slow paths); ibc = 1 / (1 - beta^t) from the host
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float adam1(float p, float g, float &m, float &v, float lr, float b1, float b2, float eps,
-                                       float bc1, float bc2) {
+                                       float ibc1, float ibc2) {
   m = b1 * m + (1.f - b1) * g;
   v = b2 * v + (1.f - b2) * g * g;
-  const float mh = m / bc1, vh = v / bc2;
-  return p - lr * mh / (sqrtf(vh) + eps);
+  const float mh = m * ibc1, vh = v * ibc2;
+  return p - lr * __fdividef(mh, sqrt_approx(vh) + eps);
 }
 
 struct AdamArgs {
   float4 *p[3];
   const float4 *g[3];
   float4 *m[3], *v[3];
-  float lr_mean, lr_ls, lr_q, lr_rho, b1, b2, eps, bc1, bc2;
+  float lr_mean, lr_ls, lr_q, lr_rho, b1, b2, eps, bc1, bc2;   // bc1, bc2: 1 / (1 - beta^t)
   int flags;   // GEM_FLAG_NO_ROTATION / GEM_FLAG_ISOTROPIC
 };
 
@@ -201,8 +208,11 @@ __global__ void __launch_bounds__(256) k_adam(int N, AdamArgs A) {
     p.y = adam1(p.y, g.y, m.y, v.y, A.lr_q, A.b1, A.b2, A.eps, A.bc1, A.bc2);
     p.z = adam1(p.z, g.z, m.z, v.z, A.lr_q, A.b1, A.b2, A.eps, A.bc1, A.bc2);
     p.w = adam1(p.w, g.w, m.w, v.w, A.lr_q, A.b1, A.b2, A.eps, A.bc1, A.bc2);
-    const float n = sqrtf(p.x * p.x + p.y * p.y + p.z * p.z + p.w * p.w);
-    if (n > 0.f) { p.x /= n; p.y /= n; p.z /= n; p.w /= n; }
+    const float n2 = p.x * p.x + p.y * p.y + p.z * p.z + p.w * p.w;
+    if (n2 > 0.f) {   // q / |q| (|q| = 1 to ~1e-7 after)
+      const float r = rsqrtf(n2);
+      p.x *= r; p.y *= r; p.z *= r; p.w *= r;
+    }
   }
   A.p[arr][j] = p;
   A.m[arr][j] = m;
@@ -242,7 +252,7 @@ void launch_adam(int N, float4 *p_mr, float4 *p_ls, float4 *p_q, const float4 *g
   A.m[0] = m_mr; A.m[1] = m_ls; A.m[2] = m_q;
   A.v[0] = v_mr; A.v[1] = v_ls; A.v[2] = v_q;
   A.lr_mean = lr_mean; A.lr_ls = lr_ls; A.lr_q = lr_q; A.lr_rho = lr_rho;
-  A.b1 = b1; A.b2 = b2; A.eps = eps; A.bc1 = bc1; A.bc2 = bc2;
+  A.b1 = b1; A.b2 = b2; A.eps = eps; A.bc1 = 1.f / bc1; A.bc2 = 1.f / bc2;   // (reciprocals)
   dim3 grid((N + 255) / 256, 3);
   k_adam<<<grid, 256, 0, s>>>(N, A);
   ++launches;
