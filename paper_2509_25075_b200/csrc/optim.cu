@@ -20,14 +20,15 @@ __device__ __forceinline__ void finalize_j(int j, int no_rot, float4 a0, float4 
                                            float4 *__restrict__ g_ls, float4 *__restrict__ g_q, DevStats *st) {
   const float4 qq = q[j], ss = ls[j];
   const float rho = mr[j].w;
-  const float n = sqrtf(qq.x * qq.x + qq.y * qq.y + qq.z * qq.z + qq.w * qq.w);
-  if (prep[j].ok == 0.0 || !(n > 0.f)) {
+  const float n2 = qq.x * qq.x + qq.y * qq.y + qq.z * qq.z + qq.w * qq.w;
+  if (prep[j].ok == 0.0 || !(n2 > 0.f)) {
     g_mr[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     g_ls[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     g_q[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
   }
-  const float w = qq.x / n, x = qq.y / n, y = qq.z / n, z = qq.w / n;
+  const float inv = rsqrtf(n2);   // 1 / |q| (MUFU: the gradient's parity is 1e-4)
+  const float w = qq.x * inv, x = qq.y * inv, y = qq.z * inv, z = qq.w * inv;
   float R[3][3];
   R[0][0] = 1.f - 2.f * (y * y + z * z); R[0][1] = 2.f * (x * y - w * z); R[0][2] = 2.f * (x * z + w * y);
   R[1][0] = 2.f * (x * y + w * z); R[1][1] = 1.f - 2.f * (x * x + z * z); R[1][2] = 2.f * (y * z - w * x);
@@ -59,7 +60,6 @@ __device__ __forceinline__ void finalize_j(int j, int no_rot, float4 a0, float4 
   float dz = 2.f * (-2.f * z * dR[0][0] - w * dR[0][1] + x * dR[0][2] + w * dR[1][0] - 2.f * z * dR[1][1] +
                     y * dR[1][2] + x * dR[2][0] + y * dR[2][1]);
   const float dot = dw * w + dx * x + dy * y + dz * z;
-  const float inv = 1.f / n;
   const float4 gq = make_float4((dw - dot * w) * inv, (dx - dot * x) * inv, (dy - dot * y) * inv, (dz - dot * z) * inv);
   g_mr[j] = make_float4(a0.y, a0.z, a0.w, a0.x);
   g_ls[j] = make_float4(ds[0], ds[1], ds[2], 0.f);
@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(10 * kRfG) k_reduce_finalize(int nchunk, int N
 #pragma unroll
   for (int m = 0; m < 10; ++m) v[m] = sv[m][jj];
   const float rho = mr[j].w;
-  finalize_j(j, no_rot, make_float4(rho != 0.f ? v[0] / rho : 0.f, v[1], v[2], v[3]), make_float4(v[4], v[5], v[6], v[7]),
-             make_float4(v[8], v[9], 0.f, 0.f), prep, mr, ls, q, g_mr, g_ls, g_q, st);
+  finalize_j(j, no_rot, make_float4(rho != 0.f ? __fdividef(v[0], rho) : 0.f, v[1], v[2], v[3]),
+             make_float4(v[4], v[5], v[6], v[7]), make_float4(v[8], v[9], 0.f, 0.f), prep, mr, ls, q, g_mr, g_ls, g_q,
+             st);
 }
 
 // The same with 128-bit loads (N % 4 == 0): one block per 128 Gaussians, warp k sums component k
@@ -155,8 +156,9 @@ __global__ void __launch_bounds__(320) k_reduce_finalize4(int nchunk, int N, int
 #pragma unroll
   for (int m = 0; m < 10; ++m) v[m] = sv[m][jj];
   const float rho = mr[j].w;
-  finalize_j(j, no_rot, make_float4(rho != 0.f ? v[0] / rho : 0.f, v[1], v[2], v[3]), make_float4(v[4], v[5], v[6], v[7]),
-             make_float4(v[8], v[9], 0.f, 0.f), prep, mr, ls, q, g_mr, g_ls, g_q, st);
+  finalize_j(j, no_rot, make_float4(rho != 0.f ? __fdividef(v[0], rho) : 0.f, v[1], v[2], v[3]),
+             make_float4(v[4], v[5], v[6], v[7]), make_float4(v[8], v[9], 0.f, 0.f), prep, mr, ls, q, g_mr, g_ls, g_q,
+             st);
 }
 
 // MUFU square root and reciprocal (a few ulp in the step lr m^ / (sqrt(v^) + eps): far below the
