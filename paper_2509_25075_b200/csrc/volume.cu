@@ -4,10 +4,11 @@
 //
 // Per Gaussian: fp64 Sigma (canonical O3 order, as in a1) -> integer k-sigma
 // voxel box and fp32 Sigma^-1; bin into 8^3 bricks (count, scan, fill); then
-// persistent CTAs zero the empty bricks and render each non-empty one: its
-// list sorted by Gaussian id, one warp per 4^3 sub-brick, one entry per lane
-// into 64 private fp32 accumulators, lane partials summed in a fixed order, so
-// the volume is bitwise reproducible.  Every voxel is written once (no memset).
+// k_vol_stage zeroes the empty bricks and writes each non-empty brick's list,
+// sorted by Gaussian id, as brick-local records, and k_vol_render evaluates
+// them: a half-warp per 4^3 sub-brick, one record per lane into 64 private
+// fp32 accumulators, lane partials summed in a fixed order, so the volume is
+// bitwise reproducible.  Every voxel is written once (no memset).
 #include "gem_internal.cuh"
 
 namespace gem {
@@ -137,7 +138,8 @@ __global__ void __launch_bounds__(64) k_vol_fill(int N, const VolRec *__restrict
 // brick's sorted record list (and of `vbox`, their boxes).
 // k_vol_render: persistent warps over the tasks (non-empty brick, pair p of its sub-bricks); the
 // half-warp h owns the 4^3 sub-brick 2p + h of the brick: it compacts the records whose box
-// meets its sub-brick (ballot, in list order) and deals them to its 16 lanes round-robin; a lane
+// meets its sub-brick (ballot over 16 boxes per step, in list order) and deals them to its 16
+// lanes round-robin; a lane
 // evaluates its record over the whole sub-brick into 64 private fp32 accumulators (the box as
 // -inf masks on the log2-exponent, one ex2 per voxel: no recurrence, no range cases).  The 16
 // partial sub-bricks are then summed in lane order through shared memory (fixed order: the
