@@ -324,6 +324,7 @@ gem_status gem_init(const gem_config *cfg, void *workspace, size_t bytes, gem_st
       cudaEventCreateWithFlags(&ctx->ev_loss, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_small, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_zero, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_obs_free[0], cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_obs_free[1], cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_sfree[0], cudaEventDisableTiming) != cudaSuccess ||
@@ -377,6 +378,7 @@ gem_status gem_destroy(gem_ctx *ctx) {
     if (ctx->ev_sfree[k]) cudaEventDestroy(ctx->ev_sfree[k]);
   }
   if (ctx->ev_small) cudaEventDestroy(ctx->ev_small);
+  if (ctx->ev_zero) cudaEventDestroy(ctx->ev_zero);
   free(ctx->ev_obs);
   for (int k = 0; k < 2 * ctx->prof_cap; ++k) cudaEventDestroy(ctx->prof_ev[k]);
   free(ctx->prof_ev);
@@ -523,6 +525,18 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
       return GEM_OK;
     };
     const float *rw = rot + 9 * (size_t)p0;
+    // device-resident inputs: the projections of this wave are cleared on the side stream while
+    // the splat and binning run, and the 8x8 render skips the empty tiles (~2/3 at R) instead of
+    // writing their zeros.  (With host inputs the extra HBM writes during the DMA of the next
+    // images cost more end to end than they save: the render writes the zeros itself.)
+    const bool cleared = !host && c.T == 8;
+    if (cleared) {
+      float *projz = proj_out ? proj_out + p0 * DD : at<float>(ctx, L.proj);
+      CK(cudaEventRecord(ctx->ev_fork, s));
+      CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      CK(cudaMemsetAsync(projz, 0, sizeof(float) * nb * DD, ctx->side));
+      CK(cudaEventRecord(ctx->ev_zero, ctx->side));
+    }
     const int64_t nh = (int64_t)nb * c.NT * c.C;
     int *ptot = hist + nh;   // per-particle entry totals (the splat adds, the scan reads)
     unsigned short *hist16 = reinterpret_cast<unsigned short *>(hist);   // 16-bit counts (<= kChunk)
@@ -547,7 +561,8 @@ gem_status gem_forward(gem_ctx *ctx, const gem_soa *params, const gem_batch *bat
       if (fs != GEM_OK) return fs;
     }
     float *proj = proj_out ? proj_out + p0 * DD : at<float>(ctx, L.proj);
-    { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, at<int>(ctx, L.lst), ids, proj, at<int>(ctx, L.ticket), s, ctx->launches); CK(cudaGetLastError()); }
+    if (cleared) CK(cudaStreamWaitEvent(s, ctx->ev_zero, 0));
+    { Prof p(ctx, s, P_RENDER_FWD); launch_render_fwd(c, nb, rec, at<int>(ctx, L.lst), ids, proj, at<int>(ctx, L.ticket), s, ctx->launches, cleared); CK(cudaGetLastError()); }
     CKF(cufftSetStream(r2c, s));
     CKF(cufftSetStream(c2r, s));
     {

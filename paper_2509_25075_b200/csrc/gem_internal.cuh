@@ -108,6 +108,7 @@ struct gem_ctx {
   cudaEvent_t ev_obs_free[2] = {nullptr, nullptr};   // the side stream's last reads of each half are done
   cudaEvent_t ev_sfree[2] = {nullptr, nullptr};      // the compute stream's last reads of each half are done
   cudaEvent_t ev_small = nullptr;                    // host mode: poses and CTFs are on the device
+  cudaEvent_t ev_zero = nullptr;                     // the wave's projections are cleared (side stream)
   float *rot_cur = nullptr;                          // the last forward's staged rotations (gem_backward)
   int n_plans;
   int fwd_live;        // a forward's lists/records/dL/dI are valid
@@ -219,7 +220,7 @@ void launch_fill(const CfgDev &c, int B, const uint2 *box, const int *base, cons
 void launch_zsort(const CfgDev &c, int B, const int *base, const float4 *mean_rho, const float *rot, int *ids,
                   const uint2 *zpair, int *tmp, int *queue, cudaStream_t s, int &launches);
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
-                       int *ticket, cudaStream_t s, int &launches);
+                       int *ticket, cudaStream_t s, int &launches, bool cleared);   // cleared: proj already zero
 void launch_ctf_params(const CfgDev &c, int B, const float *ctf, void *ctf_par, cudaStream_t s, int &launches);
 void launch_ctf_loss(const CfgDev &c, int B, const void *ctf_par, float2 *spec_hat, const float2 *spec_obs,
                      float2 *spec_pred, float2 *zout, double *loss_part, int loss_blocks, cudaStream_t s,

@@ -281,7 +281,8 @@ template <bool MK>
 __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, int B, const SplatRec *__restrict__ rec,
                                                                     const int *__restrict__ base,
                                                                     const int *__restrict__ ids,
-                                                                    float *__restrict__ proj, int *ticket) {
+                                                                    float *__restrict__ proj, int *ticket,
+                                                                    int zero_empty) {
   constexpr int T = 8;
   constexpr float nh = -0.5f * kLog2e;
   __shared__ __align__(16) float le_smem[kLeWarps * 32 * kLePitch];
@@ -327,10 +328,12 @@ __global__ void __launch_bounds__(kLeWarps * 32, 8) k_render_fwd_le(CfgDev c, in
     if ((int64_t)e > c.cap) e = (int)c.cap;
     if ((int64_t)s > c.cap) s = (int)c.cap;
     float *out = proj + (size_t)i * c.D * c.D;
-    if (s >= e) {   // empty tile: the projection is zero there
-      for (int p = lane; p < T * T; p += 32) {
-        const int u = u0 + p % T, v = v0 + p / T;
-        if (u < c.D && v < c.D) out[(size_t)v * c.D + u] = 0.f;
+    if (s >= e) {   // empty tile: the projection is zero there (or already cleared: zero_empty = 0)
+      if (zero_empty) {
+        for (int p = lane; p < T * T; p += 32) {
+          const int u = u0 + p % T, v = v0 + p / T;
+          if (u < c.D && v < c.D) out[(size_t)v * c.D + u] = 0.f;
+        }
       }
       continue;
     }
@@ -799,15 +802,15 @@ bool pixel_mask(const CfgDev &c) { return (c.flags & (GEM_FLAG_ELLIPSE | GEM_FLA
 }  // namespace
 
 void launch_render_fwd(const CfgDev &c, int B, const SplatRec *rec, const int *base, const int *ids, float *proj,
-                       int *ticket, cudaStream_t s, int &launches) {
+                       int *ticket, cudaStream_t s, int &launches, bool cleared) {
   const bool mk = pixel_mask(c);
   if (c.T == 8) {
     static int grid[2] = {0, 0};
     int &g = grid[mk ? 1 : 0];
     if (!g) g = mk ? persistent_grid(k_render_fwd_le<true>, kLeWarps * 32, 0)
                    : persistent_grid(k_render_fwd_le<false>, kLeWarps * 32, 0);
-    if (mk) k_render_fwd_le<true><<<g, kLeWarps * 32, 0, s>>>(c, B, rec, base, ids, proj, ticket);
-    else k_render_fwd_le<false><<<g, kLeWarps * 32, 0, s>>>(c, B, rec, base, ids, proj, ticket);
+    if (mk) k_render_fwd_le<true><<<g, kLeWarps * 32, 0, s>>>(c, B, rec, base, ids, proj, ticket, cleared ? 0 : 1);
+    else k_render_fwd_le<false><<<g, kLeWarps * 32, 0, s>>>(c, B, rec, base, ids, proj, ticket, cleared ? 0 : 1);
   } else {   // 16 x 16 tiles: lanes own row pairs, entries binned per pair (k_render_fwd<16>)
     if (mk) launch_fwd_t<16, true>(c, B, rec, base, ids, proj, ticket, s);
     else launch_fwd_t<16, false>(c, B, rec, base, ids, proj, ticket, s);
