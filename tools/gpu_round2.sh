@@ -3,7 +3,7 @@
 # ncu launch list of the bench command, --set full captures of the step's main kernels and of the
 # measured TMA variants.  Everything under gpurun_out/round2/ (summaries copied to profiles/r2/).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-TAG=${TAG:-r2e}
+TAG=${TAG:-r2f}
 O=gpurun_out/round2
 mkdir -p $O
 nvidia-smi > $O/nvidia-smi.txt 2>&1
