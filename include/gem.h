@@ -33,7 +33,12 @@
  * be 16-byte aligned.  libgem performs no device allocation after gem_init
  * other than cuFFT plan objects for new batch sizes (their work area comes
  * from the caller's workspace).  A context serves one thread; every call is
- * asynchronous on the given stream unless documented as synchronous.
+ * asynchronous on the given stream unless documented as synchronous.  Inside a
+ * call libgem also uses internal streams (a side stream for the observations'
+ * transform, the CTF constants, the loss reduction and the clearing of the
+ * projections; a copy stream for GEM_MEM_HOST inputs), forked from and joined
+ * back into the caller's stream: when the caller's stream has passed a call,
+ * all of that call's work is done.
  *
  * Errors: arguments are validated synchronously before any launch (no
  * exceptions cross the ABI).  Device-side conditions (list overflow, non-finite
