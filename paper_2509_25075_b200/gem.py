@@ -235,16 +235,18 @@ class Trainer:
         self.v = SoA.zeros(N, dev)
         self.t = 0
         self.group = group
-        self.global_loss = self.flat[12 * N: 12 * N + 1]   # sum over ranks after each step (fp32)
+        # with more than one rank: the loss summed over ranks after each step (fp32), all-reduced
+        # with the gradient; one rank has its total in train_step's returned loss[-1]
+        self.global_loss = self.flat[12 * N: 12 * N + 1]
 
     def train_step(self, rot, shift, ctf, observed, host=False, loss=None):
         g = self.step_ctx
         loss = g.forward(self.params, rot, shift, ctf, observed, loss=loss, host=host)
         g.backward(self.params, self.grad)
-        with torch.cuda.stream(g.stream) if self.flat.is_cuda else _nullctx():
-            self.global_loss.copy_(loss[-1:], non_blocking=True)   # the rank's total, appended
-            if _world(self.group) > 1:
-                allreduce_flat(self.flat, self.group)                # gradient + loss: one collective
+        if _world(self.group) > 1:
+            with torch.cuda.stream(g.stream) if self.flat.is_cuda else _nullctx():
+                self.global_loss.copy_(loss[-1:], non_blocking=True)   # the rank's total, appended
+                allreduce_flat(self.flat, self.group)                  # gradient + loss: one collective
         self.t += 1
         g.step(self.params, self.grad, self.m, self.v, self.t)
         return loss
